@@ -1,0 +1,403 @@
+#!/usr/bin/env python3
+"""bench.py -- REFT snapshot-and-protect on B200 (driver contract).
+
+One step = one full snapshot+protect of the rank's registered state: gather-pack
+kernel -> (N >= 2: rotated XOR parity over NVLink P2P) -> copy-engine D2H into the
+ongoing pinned host image -> commit on every rank (ckpt_snapshot + ckpt_wait).
+
+  python bench.py [--gpus N --steps K --warmup W] [--config c2_7b_tp8] [--impl reference]
+
+N = 1 runs snapshot only (a group of one has no redundancy); N >= 2 is launched under
+torchrun, one process per GPU, and the N ranks form one protection group (m = N).
+value = total state bytes committed by all ranks per second (GB/s, weak scaling).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "snapshot+parity GB/s per GPU at 1/2/4/8 B200; co-running GEMM slowdown %"
+NVLINK_PEAK_GBS = 770.0  # B200_PROFILING.md: measured peer copy per direction (nominal 900)
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=8)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    p.add_argument("--config", default="c2_7b_tp8")
+    p.add_argument("--bucket", type=int, default=64 << 20)
+    p.add_argument("--n-slots", type=int, default=4)
+    p.add_argument("--unit", type=int, default=64 << 10)
+    p.add_argument("--pack", default="lsu", choices=["lsu", "tma"])
+    p.add_argument("--no-corun", action="store_true", help="skip the co-running GEMM measurement")
+    p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--cpu-seconds", type=float, default=12.0)
+    return p.parse_args()
+
+
+def env_rank():
+    return (int(os.environ.get("RANK", 0)), int(os.environ.get("LOCAL_RANK", 0)),
+            int(os.environ.get("WORLD_SIZE", 1)))
+
+
+def load_peaks():
+    try:
+        return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        return {}
+
+
+# ------------------------------------------------------------------ clocks ----------
+class Clocks:
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu: int):
+        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                                       "-lms", "200", "-i", str(gpu)], stdout=self.f, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.p = None
+
+    def stop(self):
+        if self.p is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.p.terminate()
+        self.p.wait(10)
+        rows = [r.split(", ") for r in open(self.f.name).read().strip().splitlines() if r.count(",") >= 8]
+        os.unlink(self.f.name)
+        sm = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[5 + i].strip() == "Active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(rows)}
+
+
+# ------------------------------------------------------------------ CPU oracle ------
+def oracle_sample(config: str, m: int, seconds: float, step_seed: int = 0):
+    """Time the CPU oracle (as it stands) on a bounded sample of the workload: the first
+    tensors of each of the m ranks (up to a byte budget sized for ~`seconds` of work),
+    pack (O3) and, for m >= 2, the parity of every rank (O4).  Returns (GB/s of state,
+    sample description)."""
+    import numpy as np
+
+    import oracle
+    import synth
+
+    def run(budget):
+        imgs, tot = [], 0
+        for j in range(m):
+            specs = synth.config_tensors(config, j)
+            ts, acc = [], 0
+            for t, s in enumerate(specs):
+                if acc >= budget:
+                    break
+                n = min(s.nbytes, budget - acc)
+                ts.append(synth.fill(synth.SEED + step_seed, j, t, n))
+                acc += n
+            off, L = oracle.layout([x.size for x in ts])
+            imgs.append((ts, off, L))
+            tot += acc
+        Ls = max(x[2] for x in imgs)
+        Lstar, u = oracle.common_length([x[2] for x in imgs], 65536) if m > 1 else (Ls, 65536)
+        t0 = time.perf_counter()
+        Ds = [oracle.pack(ts, off, Lstar) for ts, off, _ in imgs]
+        if m > 1:
+            for r in range(m):
+                oracle.encode(Ds, u, r)
+        dt = time.perf_counter() - t0
+        return tot, dt
+
+    tot, dt = run(32 << 20)
+    rate = tot / dt
+    budget = int(min(max(rate * seconds / m, 32 << 20), 3 << 30))
+    tot, dt = run(budget)
+    desc = (f"oracle pack{' + rotated XOR parity of every rank' if m > 1 else ''} of the first "
+            f"{budget / 2**20:.0f} MiB of each of {m} rank(s) of {config} (1 thread, gcc -O2)")
+    return tot / dt / 1e9, desc, tot, dt
+
+
+def reference_arm(a, rank, world):
+    if rank != 0:
+        return 0
+    m = max(world, a.gpus)
+    vals, descs = [], None
+    per = max(a.cpu_seconds / max(a.steps, 1), 2.0)
+    for i in range(a.warmup):
+        oracle_sample(a.config, m, min(per, 2.0), step_seed=i)
+    t_all, b_all = 0.0, 0
+    for i in range(a.steps):
+        gbs, descs, tot, dt = oracle_sample(a.config, m, per, step_seed=100 + i)
+        vals.append(gbs)
+        t_all += dt
+        b_all += tot
+    value = b_all / t_all / 1e9
+    line = {"impl": "reference", "metric": METRIC, "value": round(value, 4), "unit": "GB/s", "n_gpus": m,
+            "steps": a.steps, "warmup": a.warmup, "ms_per_step": round(t_all / a.steps * 1e3, 3),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u8", "data": "synthetic",
+            "config": {"workload": a.config, "m": m, "sample": descs},
+            "cpu_baseline": {"value": round(value, 4), "unit": "GB/s", "cores": 1, "kind": "oracle", "sample": descs},
+            "e2e": {"value": round(value, 4), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ------------------------------------------------------------------ our arm ---------
+def main():
+    a = parse()
+    rank, local, world = env_rank()
+    if a.impl == "reference":
+        return reference_arm(a, rank, world)
+    import torch
+    import torch.distributed as dist
+
+    from paper_2310_12670_b200 import build as B
+    from paper_2310_12670_b200 import ckpt as C
+    from synth.gpu import descriptors, make_rank_state
+
+    if rank == 0 and not os.path.exists(C.LIB_PATH):
+        B.build()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    N = world
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    def allmax(x):
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def allsum(x):
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.SUM)
+        return float(t.item())
+
+    specs, ts = make_rank_state(a.config, rank, dev)
+    S = sum(s.nbytes for s in specs)
+    flags = C.CKPT_OPT_TIMING | (C.CKPT_OPT_TMA_PACK if a.pack == "tma" else 0)
+    opts = C.ckpt_options_default(n_slots=a.n_slots, bucket_bytes=a.bucket, stripe_unit=a.unit, flags=flags)
+    ctx = C.ckpt_create(local, opts)
+    t_setup = time.perf_counter()
+    C.ckpt_register(ctx, descriptors(ts, specs), {"rank": rank, "world": world, "local_rank": local,
+                                                  "local_world": world, "tp_rank": rank, "tp_size": 8,
+                                                  "pp_rank": 0, "pp_size": 1, "dp_rank": 0, "dp_size": 1})
+    if world > 1:
+        C.protect_ipc(ctx)
+    else:
+        C.ckpt_protect(ctx, 1, 0)  # EUNAVAIL: snapshot only, allocates the host arena
+    t_setup = time.perf_counter() - t_setup
+    g = C.ckpt_geometry(ctx)
+    m = g["m"]
+    stream = torch.cuda.current_stream()
+
+    # host-link roofline, measured live: pinned D2H of 1 GiB, all ranks at once
+    hb = torch.empty(1 << 30, dtype=torch.uint8, pin_memory=True)
+    db = torch.empty(1 << 30, dtype=torch.uint8, device=dev)
+    best = 0.0
+    barrier()
+    for _ in range(3):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        hb.copy_(db, non_blocking=True)
+        e1.record()
+        e1.synchronize()
+        best = max(best, (1 << 30) / e0.elapsed_time(e1) / 1e6)
+    d2h_peak = best
+    del db
+
+    def step():
+        sid = C.ckpt_snapshot(ctx, a.bucket, stream)
+        C.ckpt_wait(ctx, sid)
+
+    for _ in range(a.warmup):
+        step()
+    C.ckpt_stats_reset(ctx)
+    barrier()
+    torch.cuda.synchronize()
+    clk = Clocks(local)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(a.steps):
+        step()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    barrier()
+    clocks = clk.stop()
+    t_ms = allmax(e0.elapsed_time(e1))
+    st = C.ckpt_get_stats(ctx)
+    total_state = allsum(S) * a.steps
+    value = total_state / (t_ms / 1e3) / 1e9
+    wire = st["d2h_bytes"] / (e0.elapsed_time(e1) / 1e3) / 1e9  # this rank's host-link GB/s
+
+    # dominant kernel roofline (launch durations timed with events on its stream)
+    peaks = load_peaks()
+    hbm_peak = peaks.get("hbm_gbs", 6650.0)
+    kern = []
+    if st["pack_launches"]:
+        per = st["pack_bytes"] / st["pack_launches"]
+        dur = st["pack_ms"] / st["pack_launches"]
+        kern.append(("pack", st["pack_ms"], {"bound": "hbm", "achieved": per / dur / 1e6, "peak": hbm_peak,
+                                             "unit": "GB/s", "kernel": "pack_kernel" if a.pack == "lsu" else "pack_tma_kernel",
+                                             "bytes_per_launch": per, "avg_launch_us": dur * 1e3,
+                                             "launches": st["pack_launches"],
+                                             "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy r+w)"}))
+    if st["xor_launches"]:
+        per = st["xor_bytes_in"] / st["xor_launches"]
+        dur = st["xor_ms"] / st["xor_launches"]
+        kern.append(("xor", st["xor_ms"], {"bound": "nvlink", "achieved": per / dur / 1e6, "peak": NVLINK_PEAK_GBS,
+                                           "unit": "GB/s", "kernel": "xor_kernel<m-1>", "bytes_per_launch": per,
+                                           "avg_launch_us": dur * 1e3, "launches": st["xor_launches"],
+                                           "peak_source": "B200_PROFILING.md measured peer copy 770 GB/s/direction"}))
+    kern.sort(key=lambda x: -x[1])
+    roof = kern[0][2] if kern else None
+    if roof:
+        roof["frac"] = roof["achieved"] / roof["peak"]
+        tr_path = os.path.join(ROOT, "profiles", f"traffic_{roof['kernel'].split('<')[0]}_{a.config}.json")
+        roof["traffic"] = json.load(open(tr_path)).get("bytes_per_launch") if os.path.exists(tr_path) else None
+        for k in ("achieved", "frac", "avg_launch_us"):
+            roof[k] = round(roof[k], 4)
+    others = {k: {kk: (round(vv, 4) if isinstance(vv, float) else vv) for kk, vv in d.items()} for k, _, d in kern[1:]}
+    launches = st["pack_launches"] + st["xor_launches"]
+
+    # co-running bf16 GEMM (the O_in-mem analog, P.234; HAS layer 2, P.423)
+    corun = None
+    if not a.no_corun:
+        corun = gemm_corun(torch, C, ctx, stream, a.bucket, barrier, allmax, dev)
+
+    # e2e through the public API: load (H2D of the completed image into the tensors)
+    # + snapshot + commit (D2H), host wall clock, max over ranks
+    e2e = None
+    if not a.no_e2e:
+        C.ckpt_stats_reset(ctx)
+        barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for _ in range(a.steps):
+            C.ckpt_load(ctx, stream)
+            step()
+        torch.cuda.synchronize()
+        barrier()
+        te = allmax(time.perf_counter() - t0)
+        st2 = C.ckpt_get_stats(ctx)
+        e2e = {"value": round(allsum(S) * a.steps / te / 1e9, 4), "unit": "GB/s",
+               "h2d_bytes_per_step": int(st2["h2d_bytes"] // a.steps),
+               "d2h_bytes_per_step": int(st2["d2h_bytes"] // a.steps),
+               "what": "ckpt_load (restore from the completed host image) + ckpt_snapshot + ckpt_wait per step, "
+                       "host wall clock, max over ranks"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not a.no_cpu_baseline:
+        gbs, desc, _, _ = oracle_sample(a.config, 1, a.cpu_seconds)
+        cpu = {"value": round(gbs, 4), "unit": "GB/s", "cores": 1, "kind": "oracle", "sample": desc}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": round(value, 3), "unit": "GB/s", "n_gpus": N, "steps": a.steps,
+            "warmup": a.warmup, "ms_per_step": round(t_ms / a.steps, 3), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "u8", "data": "synthetic",
+            "config": {"workload": a.config, "state_bytes_per_gpu": S, "tensors_per_gpu": len(specs),
+                       "m": m, "L_star": g["L_star"], "stripe_unit": g["unit"], "bucket_bytes": a.bucket,
+                       "n_slots": a.n_slots, "pack": a.pack,
+                       "l2": f"inputs {S / 1e9:.2f} GB/GPU >> 126 MB L2; no flush needed"},
+            "per_gpu_gbs": round(value / N, 3),
+            "host_link": {"achieved_wire_gbs_rank0": round(wire, 3), "peak_d2h_gbs_rank0_measured": round(d2h_peak, 3),
+                          "frac": round(wire / d2h_peak, 4),
+                          "note": "binding roofline of the whole step: pinned D2H of data + parity"},
+            "roofline": roof, "other_kernels": others,
+            "gpu_launches": int(allsum(launches)),
+            "clocks": clocks,
+            "e2e": e2e, "cpu_baseline": cpu, "gemm_corun": corun,
+            "setup_s_rank0": round(t_setup, 2),
+        }
+        print(json.dumps(line), flush=True)
+    C.ckpt_destroy(ctx)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def gemm_corun(torch, C, ctx, stream, bucket, barrier, allmax, dev):
+    """bf16 8192^3 GEMMs back to back on a HIGH-priority stream; slowdown while a
+    snapshot runs on the library's low-priority streams.  Interleaved A/B x3."""
+    n = 8192
+    A = torch.randn(n, n, dtype=torch.bfloat16, device=dev)
+    Bm = torch.randn(n, n, dtype=torch.bfloat16, device=dev)
+    hi = torch.cuda.Stream(device=dev, priority=-5)
+    # size the GEMM window to ~1.5x one snapshot
+    with torch.cuda.stream(hi):
+        for _ in range(3):
+            torch.matmul(A, Bm)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(hi)
+    with torch.cuda.stream(hi):
+        for _ in range(10):
+            torch.matmul(A, Bm)
+    e1.record(hi)
+    e1.synchronize()
+    per = e0.elapsed_time(e1) / 10
+    sid = C.ckpt_snapshot(ctx, bucket, stream)
+    C.ckpt_wait(ctx, sid)
+    snap_ms = C.ckpt_get_stats(ctx)["last_snapshot_ms"] or 250.0
+    iters = int(max(20, 1.5 * snap_ms / per))
+
+    def window(with_snap):
+        barrier()
+        torch.cuda.synchronize()
+        s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        sid = None
+        if with_snap:
+            sid = C.ckpt_snapshot(ctx, bucket, stream)
+        s0.record(hi)
+        with torch.cuda.stream(hi):
+            for _ in range(iters):
+                torch.matmul(A, Bm)
+        s1.record(hi)
+        if sid is not None:
+            C.ckpt_wait(ctx, sid)
+        s1.synchronize()
+        snap = C.ckpt_get_stats(ctx)["last_snapshot_ms"] if with_snap else None
+        return allmax(s0.elapsed_time(s1)), snap
+
+    alone, withs, snaps = [], [], []
+    for _ in range(3):
+        alone.append(window(False)[0])
+        w, s = window(True)
+        withs.append(w)
+        snaps.append(s)
+    ta, tw = statistics.median(alone), statistics.median(withs)
+    flops = 2 * n ** 3 * iters
+    return {"slowdown_pct": round((tw / ta - 1) * 100, 3), "gemm_ms_alone": round(ta, 3),
+            "gemm_ms_with_snapshot": round(tw, 3), "gemm_iters": iters,
+            "gemm_tflops_alone": round(flops / ta / 1e9, 1),
+            "snapshot_ms_while_corunning": round(statistics.median(snaps), 3),
+            "snapshot_ms_alone": round(snap_ms, 3),
+            "window": "whole GEMM window (>= 1.5x snapshot), median of 3 interleaved A/B, max over ranks"}
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,268 @@
+/*
+ * ckpt.h -- C ABI of libreft_ckpt: REFT snapshot-and-protect on B200 (sm_100a).
+ *
+ * REFT (arXiv 2310.12670) keeps training state in host memory as an in-memory
+ * checkpoint ("snapshot", PAPER.md P.553-554) and protects it against the loss of
+ * one member of a group with XOR parity ("Asynchronous Erasure Coding", Eq 1,
+ * P.474-477; decode Eq 2, P.481-484; REFT-load, P.543-546).  This library is the
+ * data-parallel hot path of that method, B200-native:
+ *
+ *   ckpt_register  -> plan: every registered tensor gets an A-aligned offset in a
+ *                     packed image of L_j bytes (reading Q6)
+ *   ckpt_protect   -> bind a node group of m ranks (one GPU each); later snapshots
+ *                     also build rotated XOR parity (Q3/Q4) over NVLink P2P
+ *   ckpt_snapshot  -> gather-pack (kernel) -> [parity encode (kernel, peer reads)]
+ *                     -> copy-engine D2H into the ONGOING pinned host image
+ *   ckpt_wait      -> completion on every member, then commit ongoing -> completed
+ *                     (P.553 "the completed snapshot is replaced by the new copy")
+ *   ckpt_rebuild   -> rebuild a lost member's completed image from the survivors'
+ *                     completed images and parity (Eq 2; REFT-load step 3, P.545)
+ *   ckpt_load      -> H2D of the completed image + unpack into the tensors (P.545
+ *                     step 1, "load its checkpoint shard from local Host memory")
+ *
+ * Layout of the images (identical to the oracle):
+ *   D_j  : uint8[L*]        packed image of rank j; tensor t at off_j(t); zero pad.
+ *   P_r  : uint8[L* /(m-1)]  parity of rank r; for stripe s (= (m-1) units of u bytes)
+ *          P_r[s*u + i] = XOR_{j != r} D_j[s*(m-1)*u + sigma(r,j)*u + i],
+ *          sigma(r,j) = r - [r > j].   L* = align_up(max_j L_j, (m-1)*u).
+ *
+ * Conventions.  Every function returns CKPT_OK (0) or a negative CKPT_E* code and
+ * never throws.  ckpt_last_error() returns a thread-local message for the last
+ * failure on the calling thread.  A context is not thread-safe.  The caller owns
+ * the registered device tensors (borrowed: they must stay allocated and unmoved
+ * until ckpt_destroy) and the process group; the library owns its device staging,
+ * parity buffers, peer mappings and the pinned host arena.  Asynchronous CUDA
+ * errors are sticky on the context and surface at ckpt_wait / ckpt_load /
+ * ckpt_rebuild as CKPT_ECUDA.  There is no CPU fallback: without a CUDA device
+ * every device-touching call returns CKPT_ECUDA.
+ */
+#ifndef REFT_CKPT_H
+#define REFT_CKPT_H
+
+#include <stdint.h>
+#include <stddef.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- status codes ---------------------------------------------------------------- */
+#define CKPT_OK               0
+#define CKPT_EINVAL          (-1)  /* bad argument (null, zero size, misaligned option)   */
+#define CKPT_ECUDA           (-2)  /* CUDA runtime/driver error (sticky once async)       */
+#define CKPT_ENOMEM          (-3)  /* device or pinned host allocation failed             */
+#define CKPT_ESTATE          (-4)  /* call not valid in the context's current state       */
+#define CKPT_EUNAVAIL        (-5)  /* protection unavailable: m = 1 (SPEC S.314)          */
+#define CKPT_EMISMATCH       (-6)  /* group members disagree on geometry (digest)         */
+#define CKPT_EPEER           (-7)  /* peer mapping (CUDA IPC open / P2P) failed           */
+#define CKPT_EBUSY           (-8)  /* previous snapshot not yet waited                    */
+#define CKPT_ENOSNAP         (-9)  /* no completed snapshot to load or rebuild from       */
+#define CKPT_EUNRECOVERABLE  (-10) /* more losses than the code tolerates (P.460, S.334)  */
+
+/* ---- options ---------------------------------------------------------------------- */
+#define CKPT_OPT_TIMING      0x1u  /* time every pack/xor launch with CUDA events (stats) */
+#define CKPT_OPT_TMA_PACK    0x2u  /* pack via cp.async.bulk (TMA 1-D) through SMEM       */
+#define CKPT_OPT_LSU_PACK    0x4u  /* force the 128-bit LDG/STG pack                      */
+
+typedef struct ckpt_options {
+    uint32_t struct_size;   /* sizeof(ckpt_options); set by ckpt_options_default       */
+    uint32_t align;         /* A: packed segment alignment, power of 2 in [16, 4096];
+                               default 256 (reading Q6)                                  */
+    uint64_t stripe_unit;   /* u: bytes, multiple of 16; default 65536 (Q4);
+                               0 = one stripe, u = L* /(m-1) (SPEC S.378)                 */
+    uint64_t bucket_bytes;  /* ring slot capacity / default bucket size; default 64 MiB */
+    uint32_t n_slots;       /* device staging ring slots (>= 2); 0 = full device copy:
+                               staging holds the whole image, the fence releases the
+                               tensors after the pack alone                              */
+    uint32_t host_buffers;  /* 2 = ongoing + completed (P.553-554, default); 1 = single
+                               buffer (commit still atomic w.r.t. ckpt_wait, but a
+                               failed snapshot destroys the previous image)              */
+    int32_t  priority;      /* CUDA stream priority of the library's streams; default
+                               = the device's LEAST priority (so training runs first)   */
+    uint32_t max_ctas;      /* CTA budget of one pack/xor launch; 0 = 2 x SM count      */
+    uint32_t flags;         /* CKPT_OPT_*                                               */
+    uint32_t reserved[7];
+} ckpt_options;
+
+/* ---- registered tensors and layout -------------------------------------------------- */
+#define CKPT_DTYPE_BYTES 0u
+#define CKPT_DTYPE_BF16  1u
+#define CKPT_DTYPE_FP16  2u
+#define CKPT_DTYPE_FP32  3u
+#define CKPT_ROLE_PARAM      0u
+#define CKPT_ROLE_MASTER     1u
+#define CKPT_ROLE_EXP_AVG    2u
+#define CKPT_ROLE_EXP_AVG_SQ 3u
+#define CKPT_ROLE_OTHER      4u
+#define CKPT_TENSOR_REPLICATED 0x1u  /* TP-replicated (e.g. RMSNorm); saved anyway (Q9) */
+
+typedef struct ckpt_tensor {
+    void       *dev_ptr;   /* device address on the context's device; any alignment   */
+    uint64_t    nbytes;    /* > 0                                                       */
+    uint32_t    dtype;     /* CKPT_DTYPE_*: informational; bytes are copied raw (Q7)   */
+    uint32_t    role;      /* CKPT_ROLE_*: informational                                */
+    uint32_t    flags;     /* CKPT_TENSOR_*                                             */
+    uint32_t    reserved;
+    const char *name;      /* optional, copied                                          */
+} ckpt_tensor;
+
+typedef struct ckpt_layout {   /* the hybrid-parallel position of this rank (P.359-371) */
+    int32_t rank, world, local_rank, local_world;
+    int32_t tp_rank, tp_size, pp_rank, pp_size, dp_rank, dp_size;
+} ckpt_layout;
+
+/* ---- groups --------------------------------------------------------------------------- */
+#define CKPT_HANDLE_BYTES 1024u   /* size of one exported handle blob                   */
+#define CKPT_MAX_GROUP    8u      /* m <= 8: one 8 x B200 node (reading Q1)   */
+#define CKPT_GROUP_IPC    0u      /* one process per GPU; peers mapped with CUDA IPC,
+                                     per-bucket ordering by stream memory operations    */
+#define CKPT_GROUP_LOCAL  1u      /* all m contexts in this process (possibly the same
+                                     device); ordering by CUDA events; the group's
+                                     snapshot is issued by the last member's call        */
+
+typedef struct ckpt_ctx ckpt_ctx;
+
+typedef struct ckpt_group {
+    uint32_t         m;          /* group size, 1 <= m <= CKPT_MAX_GROUP                 */
+    uint32_t         my_index;   /* this context's member index in [0, m)               */
+    uint32_t         transport;  /* CKPT_GROUP_IPC or CKPT_GROUP_LOCAL                  */
+    uint32_t         reserved;
+    const void      *handles;    /* IPC: m * CKPT_HANDLE_BYTES blobs from
+                                    ckpt_export_handle, in member order                 */
+    ckpt_ctx *const *members;    /* LOCAL: the m contexts, in member order              */
+} ckpt_group;
+
+typedef struct ckpt_stats {      /* cumulative since ckpt_stats_reset                    */
+    uint64_t snapshots, loads, rebuilds;
+    uint64_t pack_launches, xor_launches, unpack_launches, rebuild_launches;
+    uint64_t pack_bytes;         /* algorithmic: bytes read + written by pack kernels    */
+    uint64_t xor_bytes_in;       /* algorithmic: peer bytes read by encode kernels       */
+    uint64_t xor_bytes_out;      /* parity bytes written                                 */
+    uint64_t d2h_bytes, h2d_bytes;
+    double   pack_ms, xor_ms, unpack_ms, rebuild_ms; /* summed launch durations
+                                    (only with CKPT_OPT_TIMING)                          */
+    double   last_snapshot_ms;   /* capture event -> last D2H event of the last snapshot
+                                    (only with CKPT_OPT_TIMING)                          */
+} ckpt_stats;
+
+/* ---- lifecycle ------------------------------------------------------------------------- */
+
+/* Fill *o with defaults (A = 256, u = 64 KiB, bucket = 64 MiB, n_slots = 4, two host
+ * buffers, least stream priority).  Never fails for a non-null o. */
+void ckpt_options_default(ckpt_options *o);
+
+/* Create a context bound to CUDA device `device` (one context per rank).  o may be
+ * NULL for defaults.  Errors: EINVAL (bad option), ECUDA (no such device / no CUDA),
+ * ENOMEM. */
+int ckpt_create(int device, const ckpt_options *o, ckpt_ctx **out);
+
+/* Destroy: waits for outstanding work, unmaps peers, frees everything the library
+ * owns.  NULL is a no-op. */
+int ckpt_destroy(ckpt_ctx *ctx);
+
+/* Register the rank's state (PAPER.md "Global Parameter Sharding", P.369-371: this
+ * rank's shard W_n/m -- here the TP/PP shard it holds).  Builds the packing plan:
+ * tensor t at off(t) = align_up(off(t-1) + nbytes(t-1), A), L_j = align_up(end, A)
+ * (reading Q6), and allocates the device staging.  `tensors` is copied; the device
+ * buffers are borrowed.  Registration is once per context.
+ * Errors: EINVAL (null, n = 0, nbytes = 0, pointer not on the device), ESTATE
+ * (already registered), ENOMEM. */
+int ckpt_register(ckpt_ctx *ctx, const ckpt_tensor *tensors, uint64_t n,
+                  const ckpt_layout *layout);
+
+/* Packed length L_j of this rank (after ckpt_register) and, after ckpt_protect, the
+ * group's common length L* and effective stripe unit.  Any out pointer may be NULL. */
+int ckpt_geometry(const ckpt_ctx *ctx, uint64_t *L_local, uint64_t *L_star,
+                  uint64_t *unit, uint32_t *m);
+
+/* Offset of registered tensor t in the packed image (for host-image inspection). */
+int ckpt_tensor_offset(const ckpt_ctx *ctx, uint64_t t, uint64_t *offset);
+
+/* IPC groups: write this rank's handle blob (device ordinal, geometry digest, L_j,
+ * CUDA IPC handles of its staging and flag page) to buf; *len is in/out (>=
+ * CKPT_HANDLE_BYTES).  The caller all-gathers the blobs (e.g. torch.distributed over
+ * NCCL) and passes them to ckpt_protect.  Errors: ESTATE (not registered), EINVAL. */
+int ckpt_export_handle(ckpt_ctx *ctx, void *buf, uint64_t *len);
+
+/* Bind the group ("sharding group", P.359/P.371; here the node group, Q1).
+ * COLLECTIVE over the m members.  Computes L* and the stripe geometry, checks
+ * every member's geometry digest (A, u, ring shape), maps peers (IPC) or links
+ * contexts (LOCAL), allocates parity buffers and the host arena.  Afterwards every
+ * ckpt_snapshot also builds parity.  m = 1 allocates the arena and returns
+ * EUNAVAIL (no redundancy possible).  Errors: EINVAL, ESTATE, EMISMATCH, EPEER,
+ * ENOMEM, EUNAVAIL. */
+int ckpt_protect(ckpt_ctx *ctx, const ckpt_group *g);
+
+/* Snapshot (REFT-save).  Captures the registered tensors as of the current position
+ * of `stream` (Q10) and asynchronously packs them bucket by bucket, builds parity
+ * (if protected) and copies data and parity into the ONGOING host image on the
+ * library's low-priority streams.  bucket_bytes = 0 uses the option; it is rounded
+ * down to whole stripes ((m-1)*u bytes; A bytes when unprotected) and must not
+ * exceed the ring slot capacity.  COLLECTIVE when protected: every member passes the
+ * same bucket_bytes.  *id receives the snapshot id.  Errors: EBUSY (previous
+ * snapshot not waited), EINVAL, ESTATE (not registered), ECUDA. */
+int ckpt_snapshot(ckpt_ctx *ctx, uint64_t bucket_bytes, void *stream, uint64_t *id);
+
+/* Make `stream` wait until snapshot `id` no longer reads the registered tensors
+ * (all buckets packed) -- call before the next optimizer step mutates them. */
+int ckpt_fence(ckpt_ctx *ctx, uint64_t id, void *stream);
+
+/* Host-block until snapshot `id`'s data and parity have landed in host memory on
+ * EVERY member, then commit: ongoing -> completed (P.551-554; SPEC S.427-435).  A
+ * snapshot that failed is never committed; the previous completed image stays.
+ * Errors: ECUDA (sticky async error; commit refused), ESTATE (no such snapshot). */
+int ckpt_wait(ckpt_ctx *ctx, uint64_t id);
+
+/* Restore every registered tensor from the last COMPLETED image (H2D + unpack),
+ * ordered on `stream`; returns after enqueueing (stream-ordered, host-async).
+ * Local only: no communication.  Errors: ENOSNAP, ESTATE, ECUDA. */
+int ckpt_load(ckpt_ctx *ctx, void *stream);
+
+/* Rebuild lost member `lost_rank`'s completed image (data and its parity row) from
+ * the survivors' completed images (Eq 2, P.481-484; REFT-load step 3, P.545;
+ * reading Q11: never from live device state).  COLLECTIVE over the group and
+ * host-blocking; every member passes the same lost_rank.  Survivors H2D their
+ * completed data and parity, each row owner r != k XORs its parity with the other
+ * survivors' units (NVLink reads) and writes the result into rank k's staging (P2P
+ * stores); rank k re-encodes its parity row and D2Hs both into its completed image.
+ * Follow with ckpt_load on every member to restore tensors.
+ * Errors: EUNRECOVERABLE (m = 1, or a survivor has no completed image -- more than
+ * one loss), EINVAL, ENOSNAP, ECUDA. */
+int ckpt_rebuild(ckpt_ctx *ctx, int32_t lost_rank, void *stream);
+
+/* Failure injection for drills (Q12, hardware-loss semantics): overwrite this
+ * member's completed and ongoing host images with `poison` and mark it as having no
+ * completed snapshot (it can only be restored by ckpt_rebuild). */
+int ckpt_forget(ckpt_ctx *ctx, uint8_t poison);
+
+/* Read-only view of the completed (which = 0) or ongoing (which = 1) host image:
+ * data (L* bytes) and parity (L* /(m-1) bytes, NULL/0 when unprotected).
+ * Errors: EINVAL, ENOSNAP (which = 0 and nothing committed). */
+int ckpt_host_view(const ckpt_ctx *ctx, int which, const void **data, uint64_t *dlen,
+                   const void **parity, uint64_t *plen);
+
+/* Counters and (with CKPT_OPT_TIMING) per-kernel launch durations. */
+int ckpt_get_stats(const ckpt_ctx *ctx, ckpt_stats *out);
+int ckpt_stats_reset(ckpt_ctx *ctx);
+
+/* Messages.  ckpt_strerror never returns NULL; ckpt_last_error returns "" when the
+ * calling thread has no error recorded. */
+const char *ckpt_strerror(int code);
+const char *ckpt_last_error(void);
+
+/* Host-only planner entry (no device needed): offsets and L for a tensor list, the
+ * same rule ckpt_register applies.  Used by CPU tests of the host logic. */
+int ckpt_plan_layout(const uint64_t *nbytes, uint64_t n, uint32_t align,
+                     uint64_t *offsets, uint64_t *L);
+
+/* Host-only: L* and effective u for a group with packed lengths Lj[0..m). */
+int ckpt_plan_common(const uint64_t *Lj, uint32_t m, uint64_t unit, uint64_t *L_star,
+                     uint64_t *unit_eff);
+
+/* Library version string, e.g. "reft-ckpt 0.1 sm_100a". */
+const char *ckpt_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* REFT_CKPT_H */

@@ -1,0 +1,357 @@
+"""Thin ctypes binding of libreft_ckpt (include/ckpt.h): same names, argument
+marshalling only.  Every step of the hot path runs in the CUDA library; there is no
+CPU fallback -- importing this module on a machine without the built library raises.
+
+PyTorch is used only as plumbing: device tensors (their data pointers), CUDA streams
+(their handles) and ``torch.distributed`` for the handle exchange of IPC groups.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from typing import Iterable, Optional, Sequence
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libreft_ckpt.so")
+SYNTH_PATH = os.path.join(_HERE, "libreft_synth.so")
+
+CKPT_OK = 0
+CKPT_EINVAL = -1
+CKPT_ECUDA = -2
+CKPT_ENOMEM = -3
+CKPT_ESTATE = -4
+CKPT_EUNAVAIL = -5
+CKPT_EMISMATCH = -6
+CKPT_EPEER = -7
+CKPT_EBUSY = -8
+CKPT_ENOSNAP = -9
+CKPT_EUNRECOVERABLE = -10
+
+CKPT_OPT_TIMING = 0x1
+CKPT_OPT_TMA_PACK = 0x2
+CKPT_OPT_LSU_PACK = 0x4
+
+CKPT_DTYPE_BYTES, CKPT_DTYPE_BF16, CKPT_DTYPE_FP16, CKPT_DTYPE_FP32 = 0, 1, 2, 3
+CKPT_ROLE_PARAM, CKPT_ROLE_MASTER, CKPT_ROLE_EXP_AVG, CKPT_ROLE_EXP_AVG_SQ, CKPT_ROLE_OTHER = 0, 1, 2, 3, 4
+CKPT_TENSOR_REPLICATED = 0x1
+
+CKPT_HANDLE_BYTES = 1024
+CKPT_MAX_GROUP = 8
+CKPT_GROUP_IPC = 0
+CKPT_GROUP_LOCAL = 1
+
+_u32, _u64, _i32 = ctypes.c_uint32, ctypes.c_uint64, ctypes.c_int32
+_vp = ctypes.c_void_p
+
+
+class ckpt_options(ctypes.Structure):
+    _fields_ = [("struct_size", _u32), ("align", _u32), ("stripe_unit", _u64), ("bucket_bytes", _u64),
+                ("n_slots", _u32), ("host_buffers", _u32), ("priority", _i32), ("max_ctas", _u32),
+                ("flags", _u32), ("reserved", _u32 * 7)]
+
+
+class ckpt_tensor(ctypes.Structure):
+    _fields_ = [("dev_ptr", _vp), ("nbytes", _u64), ("dtype", _u32), ("role", _u32), ("flags", _u32),
+                ("reserved", _u32), ("name", ctypes.c_char_p)]
+
+
+class ckpt_layout(ctypes.Structure):
+    _fields_ = [(n, _i32) for n in ("rank", "world", "local_rank", "local_world", "tp_rank", "tp_size",
+                                    "pp_rank", "pp_size", "dp_rank", "dp_size")]
+
+
+class ckpt_group(ctypes.Structure):
+    _fields_ = [("m", _u32), ("my_index", _u32), ("transport", _u32), ("reserved", _u32),
+                ("handles", _vp), ("members", ctypes.POINTER(_vp))]
+
+
+class ckpt_stats(ctypes.Structure):
+    _fields_ = [(n, _u64) for n in ("snapshots", "loads", "rebuilds", "pack_launches", "xor_launches",
+                                    "unpack_launches", "rebuild_launches", "pack_bytes", "xor_bytes_in",
+                                    "xor_bytes_out", "d2h_bytes", "h2d_bytes")] + \
+               [(n, ctypes.c_double) for n in ("pack_ms", "xor_ms", "unpack_ms", "rebuild_ms", "last_snapshot_ms")]
+
+    def as_dict(self):
+        return {n: getattr(self, n) for n, _ in self._fields_}
+
+
+class CkptError(RuntimeError):
+    def __init__(self, code: int, where: str, msg: str):
+        self.code = code
+        super().__init__(f"{where}: {ckpt_strerror(code)} ({code}): {msg}")
+
+
+_lib = None
+
+
+def lib():
+    """The loaded libreft_ckpt.so (raises if it has not been built)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"{LIB_PATH} is missing: run `python -c 'import __graft_entry__ as g; g.build()'` "
+                              "(there is no CPU fallback)")
+        L = ctypes.CDLL(LIB_PATH)
+        sig = {
+            "ckpt_options_default": (None, [ctypes.POINTER(ckpt_options)]),
+            "ckpt_create": (ctypes.c_int, [ctypes.c_int, ctypes.POINTER(ckpt_options), ctypes.POINTER(_vp)]),
+            "ckpt_destroy": (ctypes.c_int, [_vp]),
+            "ckpt_register": (ctypes.c_int, [_vp, ctypes.POINTER(ckpt_tensor), _u64, ctypes.POINTER(ckpt_layout)]),
+            "ckpt_geometry": (ctypes.c_int, [_vp, ctypes.POINTER(_u64), ctypes.POINTER(_u64), ctypes.POINTER(_u64),
+                                             ctypes.POINTER(_u32)]),
+            "ckpt_tensor_offset": (ctypes.c_int, [_vp, _u64, ctypes.POINTER(_u64)]),
+            "ckpt_export_handle": (ctypes.c_int, [_vp, _vp, ctypes.POINTER(_u64)]),
+            "ckpt_protect": (ctypes.c_int, [_vp, ctypes.POINTER(ckpt_group)]),
+            "ckpt_snapshot": (ctypes.c_int, [_vp, _u64, _vp, ctypes.POINTER(_u64)]),
+            "ckpt_fence": (ctypes.c_int, [_vp, _u64, _vp]),
+            "ckpt_wait": (ctypes.c_int, [_vp, _u64]),
+            "ckpt_load": (ctypes.c_int, [_vp, _vp]),
+            "ckpt_rebuild": (ctypes.c_int, [_vp, _i32, _vp]),
+            "ckpt_forget": (ctypes.c_int, [_vp, ctypes.c_uint8]),
+            "ckpt_host_view": (ctypes.c_int, [_vp, ctypes.c_int, ctypes.POINTER(_vp), ctypes.POINTER(_u64),
+                                              ctypes.POINTER(_vp), ctypes.POINTER(_u64)]),
+            "ckpt_get_stats": (ctypes.c_int, [_vp, ctypes.POINTER(ckpt_stats)]),
+            "ckpt_stats_reset": (ctypes.c_int, [_vp]),
+            "ckpt_strerror": (ctypes.c_char_p, [ctypes.c_int]),
+            "ckpt_last_error": (ctypes.c_char_p, []),
+            "ckpt_plan_layout": (ctypes.c_int, [_vp, _u64, _u32, _vp, ctypes.POINTER(_u64)]),
+            "ckpt_plan_common": (ctypes.c_int, [_vp, _u32, _u64, ctypes.POINTER(_u64), ctypes.POINTER(_u64)]),
+            "ckpt_version": (ctypes.c_char_p, []),
+        }
+        for name, (res, args) in sig.items():
+            f = getattr(L, name)
+            f.restype = res
+            f.argtypes = args
+        _lib = L
+    return _lib
+
+
+def _check(rc: int, where: str) -> int:
+    if rc < 0:
+        raise CkptError(rc, where, ckpt_last_error())
+    return rc
+
+
+def _stream_handle(stream) -> int:
+    if stream is None:
+        import torch
+        return torch.cuda.current_stream().cuda_stream
+    if isinstance(stream, int):
+        return stream
+    return stream.cuda_stream
+
+
+# ---------------------------------------------------------------- messages ---------
+def ckpt_strerror(code: int) -> str:
+    return lib().ckpt_strerror(code).decode()
+
+
+def ckpt_last_error() -> str:
+    return lib().ckpt_last_error().decode()
+
+
+def ckpt_version() -> str:
+    return lib().ckpt_version().decode()
+
+
+# ---------------------------------------------------------------- lifecycle --------
+def ckpt_options_default(**kw) -> ckpt_options:
+    o = ckpt_options()
+    lib().ckpt_options_default(ctypes.byref(o))
+    for k, v in kw.items():
+        setattr(o, k, v)
+    return o
+
+
+def ckpt_create(device: int, options: Optional[ckpt_options] = None) -> int:
+    ctx = _vp()
+    _check(lib().ckpt_create(device, ctypes.byref(options) if options is not None else None, ctypes.byref(ctx)),
+           "ckpt_create")
+    return ctx.value
+
+
+def ckpt_destroy(ctx: int) -> None:
+    _check(lib().ckpt_destroy(ctx), "ckpt_destroy")
+
+
+_DTYPES = {"bfloat16": CKPT_DTYPE_BF16, "float16": CKPT_DTYPE_FP16, "float32": CKPT_DTYPE_FP32}
+
+
+def tensor_desc(t, role: int = CKPT_ROLE_OTHER, flags: int = 0, name: str = "") -> tuple:
+    """(ptr, nbytes, dtype, role, flags, name) of a torch tensor (must be contiguous)."""
+    if not t.is_contiguous():
+        raise ValueError("registered tensors must be contiguous")
+    return (t.data_ptr(), t.numel() * t.element_size(), _DTYPES.get(str(t.dtype).split(".")[-1], CKPT_DTYPE_BYTES),
+            role, flags, name)
+
+
+def ckpt_register(ctx: int, tensors: Sequence, layout: Optional[dict] = None) -> None:
+    """tensors: torch tensors or (ptr, nbytes, dtype, role, flags, name) tuples."""
+    arr = (ckpt_tensor * len(tensors))()
+    names = []
+    for i, t in enumerate(tensors):
+        d = t if isinstance(t, tuple) else tensor_desc(t)
+        names.append(d[5].encode() if d[5] else None)
+        arr[i] = ckpt_tensor(d[0], d[1], d[2], d[3], d[4], 0, names[-1])
+    lay = ckpt_layout(**(layout or {}))
+    _check(lib().ckpt_register(ctx, arr, len(tensors), ctypes.byref(lay)), "ckpt_register")
+
+
+def ckpt_geometry(ctx: int) -> dict:
+    a, b, c, m = _u64(), _u64(), _u64(), _u32()
+    _check(lib().ckpt_geometry(ctx, ctypes.byref(a), ctypes.byref(b), ctypes.byref(c), ctypes.byref(m)),
+           "ckpt_geometry")
+    return {"L": a.value, "L_star": b.value, "unit": c.value, "m": m.value}
+
+
+def ckpt_tensor_offset(ctx: int, t: int) -> int:
+    o = _u64()
+    _check(lib().ckpt_tensor_offset(ctx, t, ctypes.byref(o)), "ckpt_tensor_offset")
+    return o.value
+
+
+def ckpt_export_handle(ctx: int) -> bytes:
+    buf = ctypes.create_string_buffer(CKPT_HANDLE_BYTES)
+    n = _u64(CKPT_HANDLE_BYTES)
+    _check(lib().ckpt_export_handle(ctx, buf, ctypes.byref(n)), "ckpt_export_handle")
+    return buf.raw[: n.value]
+
+
+def ckpt_protect(ctx: int, m: int, my_index: int, transport: int = CKPT_GROUP_IPC,
+                 handles: Optional[bytes] = None, members: Optional[Sequence[int]] = None) -> int:
+    """Returns CKPT_OK, or CKPT_EUNAVAIL for m == 1 (snapshot-only; not an error)."""
+    g = ckpt_group(m, my_index, transport, 0, None, None)
+    keep = None
+    if handles is not None:
+        keep = ctypes.create_string_buffer(handles, len(handles))
+        g.handles = ctypes.cast(keep, _vp)
+    if members is not None:
+        keep_m = (_vp * len(members))(*members)
+        g.members = ctypes.cast(keep_m, ctypes.POINTER(_vp))
+    rc = lib().ckpt_protect(ctx, ctypes.byref(g))
+    if rc == CKPT_EUNAVAIL:
+        return rc
+    return _check(rc, "ckpt_protect")
+
+
+def ckpt_snapshot(ctx: int, bucket_bytes: int = 0, stream=None) -> int:
+    sid = _u64()
+    _check(lib().ckpt_snapshot(ctx, bucket_bytes, _stream_handle(stream), ctypes.byref(sid)), "ckpt_snapshot")
+    return sid.value
+
+
+def ckpt_fence(ctx: int, sid: int, stream=None) -> None:
+    _check(lib().ckpt_fence(ctx, sid, _stream_handle(stream)), "ckpt_fence")
+
+
+def ckpt_wait(ctx: int, sid: int) -> None:
+    _check(lib().ckpt_wait(ctx, sid), "ckpt_wait")
+
+
+def ckpt_load(ctx: int, stream=None) -> None:
+    _check(lib().ckpt_load(ctx, _stream_handle(stream)), "ckpt_load")
+
+
+def ckpt_rebuild(ctx: int, lost_rank: int, stream=None) -> None:
+    _check(lib().ckpt_rebuild(ctx, lost_rank, _stream_handle(stream)), "ckpt_rebuild")
+
+
+def ckpt_forget(ctx: int, poison: int = 0xA5) -> None:
+    _check(lib().ckpt_forget(ctx, poison), "ckpt_forget")
+
+
+def ckpt_host_view(ctx: int, which: int = 0, copy: bool = False):
+    """(data, parity) numpy uint8 arrays over the completed (0) / ongoing (1) host image.
+    Zero-copy views by default: they dangle after ckpt_destroy (pass copy=True to keep)."""
+    d, dl, p, pl = _vp(), _u64(), _vp(), _u64()
+    _check(lib().ckpt_host_view(ctx, which, ctypes.byref(d), ctypes.byref(dl), ctypes.byref(p), ctypes.byref(pl)),
+           "ckpt_host_view")
+    data = np.ctypeslib.as_array(ctypes.cast(d.value, ctypes.POINTER(ctypes.c_uint8)), shape=(dl.value,)) \
+        if dl.value else np.zeros(0, np.uint8)
+    par = np.ctypeslib.as_array(ctypes.cast(p.value, ctypes.POINTER(ctypes.c_uint8)), shape=(pl.value,)) \
+        if pl.value else None
+    if copy:
+        data = data.copy()
+        par = par.copy() if par is not None else None
+    return data, par
+
+
+def ckpt_get_stats(ctx: int) -> dict:
+    s = ckpt_stats()
+    _check(lib().ckpt_get_stats(ctx, ctypes.byref(s)), "ckpt_get_stats")
+    return s.as_dict()
+
+
+def ckpt_stats_reset(ctx: int) -> None:
+    _check(lib().ckpt_stats_reset(ctx), "ckpt_stats_reset")
+
+
+def ckpt_plan_layout(nbytes: Sequence[int], align: int = 256):
+    nb = np.ascontiguousarray(np.asarray(nbytes, dtype=np.uint64))
+    off = np.zeros(max(len(nb), 1), dtype=np.uint64)
+    L = _u64()
+    _check(lib().ckpt_plan_layout(nb.ctypes.data, len(nb), align, off.ctypes.data, ctypes.byref(L)),
+           "ckpt_plan_layout")
+    return off[: len(nb)].astype(np.int64).tolist(), L.value
+
+
+def ckpt_plan_common(Ls: Sequence[int], unit: int):
+    a = np.ascontiguousarray(np.asarray(Ls, dtype=np.uint64))
+    Ls_, ue = _u64(), _u64()
+    _check(lib().ckpt_plan_common(a.ctypes.data, len(a), unit, ctypes.byref(Ls_), ctypes.byref(ue)),
+           "ckpt_plan_common")
+    return Ls_.value, ue.value
+
+
+# ---------------------------------------------------------------- group plumbing ---
+def exchange_handles(blob: bytes, group=None) -> bytes:
+    """All-gather this rank's fixed-size handle blob over torch.distributed (NCCL or gloo);
+    returns the concatenation in group-rank order.  Handshake only."""
+    import torch
+    import torch.distributed as dist
+    assert len(blob) == CKPT_HANDLE_BYTES
+    backend = dist.get_backend(group)
+    dev = torch.device("cuda", torch.cuda.current_device()) if backend == "nccl" else torch.device("cpu")
+    mine = torch.frombuffer(bytearray(blob), dtype=torch.uint8).to(dev)
+    world = dist.get_world_size(group)
+    outs = [torch.empty_like(mine) for _ in range(world)]
+    dist.all_gather(outs, mine, group=group)
+    return b"".join(bytes(o.cpu().numpy().tobytes()) for o in outs)
+
+
+def protect_ipc(ctx: int, group=None) -> int:
+    """Collective: bind the torch.distributed group (one process per GPU of one node) as
+    the protection group; member index = rank in ``group``."""
+    import torch.distributed as dist
+    blobs = exchange_handles(ckpt_export_handle(ctx), group)
+    m, me = dist.get_world_size(group), dist.get_rank(group)
+    rc = ckpt_protect(ctx, m, me, CKPT_GROUP_IPC, handles=blobs)
+    dist.barrier(group)
+    return rc
+
+
+def protect_local(ctxs: Sequence[int]) -> None:
+    """Bind m contexts of this process (same or different devices) as one group."""
+    for i, c in enumerate(ctxs):
+        ckpt_protect(c, len(ctxs), i, CKPT_GROUP_LOCAL, members=list(ctxs))
+
+
+# ---------------------------------------------------------------- harness generator
+_synth = None
+
+
+def reft_synth_fill(ptr: int, nbytes: int, seed: int, rank: int, tensor: int, xor_mode: int = 0,
+                    stream=None) -> None:
+    """Seeded GPU fill (harness generator, include/reft_synth.h)."""
+    global _synth
+    if _synth is None:
+        if not os.path.exists(SYNTH_PATH):
+            raise ImportError(f"{SYNTH_PATH} is missing: build first")
+        _synth = ctypes.CDLL(SYNTH_PATH)
+        _synth.reft_synth_fill.restype = ctypes.c_int
+        _synth.reft_synth_fill.argtypes = [_vp, _u64, _u64, _u64, _u64, ctypes.c_int, _vp]
+    rc = _synth.reft_synth_fill(ptr, nbytes, seed, rank, tensor, xor_mode, _stream_handle(stream))
+    if rc != 0:
+        raise RuntimeError(f"reft_synth_fill failed ({rc})")

@@ -1,0 +1,377 @@
+// ckpt_kernels.cu -- sm_100a kernels of libreft_ckpt (product code).
+//
+//  * pack/unpack: gather the registered tensors into a bucket of the packed image
+//    (or scatter it back).  HBM-bound: 1 read + 1 write per state byte.  128-bit
+//    LDG/STG with UNROLL independent loads in flight per thread; a funnel-shift path
+//    keeps 128-bit stores when source and destination are misaligned mod 16 (bf16
+//    views can start at any 2-byte offset).
+//  * xor_gather: the AEC parity encode (Eq 1, P.476) and the rebuild
+//    decode (Eq 2, P.483) as one kernel: every 16-byte output word is the XOR of up
+//    to 8 input words, each from its own (possibly NVLink-peer) stream.  NVLink-bound
+//    for the encode: (m-1) peer units in per parity unit out.
+//
+// No tensor cores: the path is pure data movement.
+#include "ckpt_kernels.cuh"
+
+namespace reft {
+namespace {
+
+constexpr int kPackThreads = 512;
+constexpr int kPackUnroll = 4;
+constexpr int kXorThreads = 256;
+constexpr int kXorUnroll = 2;
+
+__device__ __forceinline__ uint4 ld_stream(const void *p) {
+    uint4 r;
+    asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+                 : "l"(p));
+    return r;
+}
+
+// Coherent (non-.nc) 128-bit load, L2 only: used for peer slots, which are rewritten
+// between launches by their owners.
+__device__ __forceinline__ uint4 ld_cg(const void *p) {
+    uint4 r;
+    asm volatile("ld.global.cg.v4.u32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+                 : "l"(p));
+    return r;
+}
+
+__device__ __forceinline__ void st_stream(void *p, const uint4 &v) {
+    asm volatile("st.global.L1::no_allocate.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x),
+                 "r"(v.y), "r"(v.z), "r"(v.w)
+                 : "memory");
+}
+
+// 16 bytes starting at byte `sh` (1..15) of the 32-byte pair (a, b).
+__device__ __forceinline__ uint4 funnel16(const uint4 &a, const uint4 &b, uint32_t sh) {
+    const uint32_t w[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+    const uint32_t q = sh >> 2, bs = (sh & 3) * 8;
+    uint4 o;
+    // q is uniform per chunk; the selects compile to predicated moves, no local memory
+    uint32_t v0 = q == 0 ? w[0] : q == 1 ? w[1] : q == 2 ? w[2] : w[3];
+    uint32_t v1 = q == 0 ? w[1] : q == 1 ? w[2] : q == 2 ? w[3] : w[4];
+    uint32_t v2 = q == 0 ? w[2] : q == 1 ? w[3] : q == 2 ? w[4] : w[5];
+    uint32_t v3 = q == 0 ? w[3] : q == 1 ? w[4] : q == 2 ? w[5] : w[6];
+    uint32_t v4 = q == 0 ? w[4] : q == 1 ? w[5] : q == 2 ? w[6] : w[7];
+    o.x = __funnelshift_r(v0, v1, bs);
+    o.y = __funnelshift_r(v1, v2, bs);
+    o.z = __funnelshift_r(v2, v3, bs);
+    o.w = __funnelshift_r(v3, v4, bs);
+    return o;
+}
+
+// Block-cooperative copy of n bytes (any alignment).
+__device__ __forceinline__ void block_copy(uint8_t *__restrict__ dst, const uint8_t *__restrict__ src,
+                                           uint64_t n) {
+    const uint32_t tid = threadIdx.x, nt = blockDim.x;
+    uint64_t head = (16 - ((uintptr_t)dst & 15)) & 15;
+    if (head > n) head = n;
+    if (tid < head) dst[tid] = src[tid];
+    dst += head;
+    src += head;
+    n -= head;
+    const uint64_t nw = n >> 4;
+    uint4 *__restrict__ d4 = reinterpret_cast<uint4 *>(dst);
+    const uint32_t sh = (uintptr_t)src & 15;
+    if (sh == 0) {
+        const uint4 *__restrict__ s4 = reinterpret_cast<const uint4 *>(src);
+        uint64_t i = tid;
+        for (; i + (kPackUnroll - 1) * nt < nw; i += kPackUnroll * nt) {
+            uint4 v[kPackUnroll];
+#pragma unroll
+            for (int u = 0; u < kPackUnroll; ++u) v[u] = ld_stream(s4 + i + u * nt);
+#pragma unroll
+            for (int u = 0; u < kPackUnroll; ++u) st_stream(d4 + i + u * nt, v[u]);
+        }
+        for (; i < nw; i += nt) st_stream(d4 + i, ld_stream(s4 + i));
+    } else {
+        // aligned 16-byte source blocks a = floor16(src) + 16 i, b = a + 16; every block
+        // read holds at least one byte of the source range, so it never crosses a page
+        const uint4 *__restrict__ s4 = reinterpret_cast<const uint4 *>(src - sh);
+        uint64_t i = tid;
+        for (; i + (kPackUnroll - 1) * nt < nw; i += kPackUnroll * nt) {
+            uint4 a[kPackUnroll], b[kPackUnroll];
+#pragma unroll
+            for (int u = 0; u < kPackUnroll; ++u) {
+                a[u] = ld_stream(s4 + i + u * nt);
+                b[u] = ld_stream(s4 + i + u * nt + 1);
+            }
+#pragma unroll
+            for (int u = 0; u < kPackUnroll; ++u) st_stream(d4 + i + u * nt, funnel16(a[u], b[u], sh));
+        }
+        for (; i < nw; i += nt) st_stream(d4 + i, funnel16(ld_stream(s4 + i), ld_stream(s4 + i + 1), sh));
+    }
+    const uint64_t tail = n & 15, t0 = nw << 4;
+    if (tid < tail) dst[t0 + tid] = src[t0 + tid];
+}
+
+__device__ __forceinline__ void block_zero(uint8_t *dst, uint64_t n) {
+    const uint32_t tid = threadIdx.x, nt = blockDim.x;
+    uint64_t head = (16 - ((uintptr_t)dst & 15)) & 15;
+    if (head > n) head = n;
+    if (tid < head) dst[tid] = 0;
+    dst += head;
+    n -= head;
+    const uint64_t nw = n >> 4;
+    uint4 *d4 = reinterpret_cast<uint4 *>(dst);
+    for (uint64_t i = tid; i < nw; i += nt) st_stream(d4 + i, make_uint4(0, 0, 0, 0));
+    const uint64_t tail = n & 15, t0 = nw << 4;
+    if (tid < tail) dst[t0 + tid] = 0;
+}
+
+__global__ void __launch_bounds__(kPackThreads) pack_kernel(const PackArgs a) {
+    for (uint64_t c = blockIdx.x; c < a.count; c += gridDim.x) {
+        const PackChunk ch = a.chunks[a.first + c];
+        const uint64_t lo = ch.dst > a.bucket_begin ? ch.dst : a.bucket_begin;
+        const uint64_t end = ch.dst + ch.nbytes;
+        const uint64_t hi = end < a.bucket_end ? end : a.bucket_end;
+        if (lo >= hi) continue;
+        uint8_t *slot = a.slot + (lo - a.bucket_begin);
+        if (ch.src == 0) {
+            if (!a.unpack) block_zero(slot, hi - lo);
+            continue;
+        }
+        uint8_t *tensor = reinterpret_cast<uint8_t *>(ch.src) + (lo - ch.dst);
+        if (a.unpack)
+            block_copy(tensor, slot, hi - lo);
+        else
+            block_copy(slot, tensor, hi - lo);
+    }
+}
+
+
+// ---------------------------------------------------------------------------------
+// TMA pack: 1-D bulk copies (cp.async.bulk) global -> SMEM -> global issued by one
+// thread per CTA, kTmaStages stages of kTmaStage bytes in flight.  A 32-thread CTA
+// with 64 KiB of SMEM moves as many bytes per SM as the 512-thread LSU kernel while
+// holding 16x fewer threads/registers -- the low-SM-footprint variant for co-running
+// with a training GEMM.  Chunks whose source and destination differ mod 16 (and the
+// < 16-byte heads/tails) go through the warp's LSU path.
+constexpr int kTmaThreads = 32;
+constexpr int kTmaStages = 4;
+constexpr uint32_t kTmaStage = 16 * 1024;
+
+__device__ __forceinline__ uint32_t smem_u32(const void *p) {
+    return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
+    asm volatile(
+        "{\n .reg .pred p;\n"
+        "WAIT_%=:\n"
+        " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        " @!p bra WAIT_%=;\n}\n" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void *smem, const void *gmem, uint32_t bytes, uint64_t *bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(smem_u32(smem)),
+        "l"(gmem), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+__device__ __forceinline__ void bulk_s2g(void *gmem, const void *smem, uint32_t bytes) {
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(gmem), "r"(smem_u32(smem)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void bulk_wait_read() {
+    asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
+}
+__device__ __forceinline__ void bulk_wait_read_n(uint32_t n) {
+    switch (n) {
+        case 0: bulk_wait_read<0>(); break;
+        case 1: bulk_wait_read<1>(); break;
+        case 2: bulk_wait_read<2>(); break;
+        default: bulk_wait_read<3>(); break;
+    }
+}
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+
+// One bulk piece: up to kTmaStage bytes of one chunk body.
+struct Piece {
+    const uint8_t *src;
+    uint8_t *dst;
+    uint32_t bytes;
+};
+
+__global__ void __launch_bounds__(kTmaThreads) pack_tma_kernel(const PackArgs a) {
+    extern __shared__ __align__(128) uint8_t smem[];
+    __shared__ __align__(8) uint64_t bars[kTmaStages];
+    const uint32_t lane = threadIdx.x;
+    if (lane == 0) {
+        for (int i = 0; i < kTmaStages; ++i) mbar_init(&bars[i], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    }
+    __syncwarp();
+    uint32_t phase = 0;      // bit i = parity to wait for on stage i
+    uint32_t issued = 0, done = 0;  // pieces loaded / stored (lane 0 only)
+    Piece ring[kTmaStages];
+    for (uint64_t c = blockIdx.x; c < a.count; c += gridDim.x) {
+        const PackChunk ch = a.chunks[a.first + c];
+        const uint64_t lo = ch.dst > a.bucket_begin ? ch.dst : a.bucket_begin;
+        const uint64_t end = ch.dst + ch.nbytes;
+        const uint64_t hi = end < a.bucket_end ? end : a.bucket_end;
+        if (lo >= hi) continue;
+        uint8_t *slot = a.slot + (lo - a.bucket_begin);
+        uint64_t n = hi - lo;
+        if (ch.src == 0) {
+            if (!a.unpack) block_zero(slot, n);
+            continue;
+        }
+        uint8_t *tensor = reinterpret_cast<uint8_t *>(ch.src) + (lo - ch.dst);
+        uint8_t *dst = a.unpack ? tensor : slot;
+        const uint8_t *src = a.unpack ? slot : tensor;
+        if ((((uintptr_t)dst ^ (uintptr_t)src) & 15) || n < 64) {
+            block_copy(dst, src, n);
+            continue;
+        }
+        uint64_t head = (16 - ((uintptr_t)dst & 15)) & 15;
+        uint64_t body = (n - head) & ~(uint64_t)15;
+        uint64_t tail = n - head - body;
+        if (lane < head) dst[lane] = src[lane];
+        if (lane < tail) dst[head + body + lane] = src[head + body + lane];
+        if (lane == 0) {
+            const uint8_t *s = src + head;
+            uint8_t *d = dst + head;
+            for (uint64_t o = 0; o < body;) {
+                const uint32_t bytes = (uint32_t)((body - o) < kTmaStage ? (body - o) : kTmaStage);
+                // at most kTmaStages-1 loads in flight: retire the oldest (wait for its
+                // load, issue its store) so one store can drain while the next loads fly
+                if (issued - done == kTmaStages - 1) {
+                    const uint32_t so = done % kTmaStages;
+                    mbar_wait(&bars[so], (phase >> so) & 1);
+                    phase ^= 1u << so;
+                    bulk_s2g(ring[so].dst, smem + so * kTmaStage, ring[so].bytes);
+                    bulk_commit();
+                    ++done;
+                }
+                const uint32_t st = issued % kTmaStages;
+                // the store of piece issued-kTmaStages (same stage) must have finished
+                // reading SMEM; stores committed after it may stay in flight
+                if (issued >= kTmaStages) bulk_wait_read_n(done + kTmaStages - 1 - issued);
+                ring[st] = Piece{s + o, d + o, bytes};
+                mbar_expect_tx(&bars[st], bytes);
+                bulk_g2s(smem + st * kTmaStage, s + o, bytes, &bars[st]);
+                ++issued;
+                o += bytes;
+            }
+        }
+    }
+    if (lane == 0) {
+        while (done < issued) {
+            const uint32_t st = done % kTmaStages;
+            mbar_wait(&bars[st], (phase >> st) & 1);
+            phase ^= 1u << st;
+            bulk_s2g(ring[st].dst, smem + st * kTmaStage, ring[st].bytes);
+            bulk_commit();
+            ++done;
+        }
+        bulk_wait_all();
+    }
+    __syncwarp();
+}
+
+// ---------------------------------------------------------------------------------
+// XOR gather.  Work is split into tiles of kXorThreads * kXorUnroll 16-byte words
+// inside one unit, so the stripe index needs one 32-bit division per tile.
+template <int NIN>
+__global__ void __launch_bounds__(kXorThreads) xor_kernel(const XorArgs a) {
+    const uint32_t words_per_unit = (uint32_t)(a.unit >> 4);
+    constexpr uint32_t kTile = kXorThreads * kXorUnroll;
+    const uint32_t tiles_per_unit = (words_per_unit + kTile - 1) / kTile;
+    const uint64_t ntiles = a.nstripes * tiles_per_unit;
+    for (uint64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+        const uint64_t s = t / tiles_per_unit;
+        const uint32_t w0 = (uint32_t)(t - s * tiles_per_unit) * kTile + threadIdx.x;
+        uint4 acc[kXorUnroll];
+        uint4 v[NIN][kXorUnroll];
+#pragma unroll
+        for (int k = 0; k < NIN; ++k) {
+            const uint64_t base = s * a.in[k].stride + a.in[k].off;
+#pragma unroll
+            for (int u = 0; u < kXorUnroll; ++u) {
+                const uint32_t w = w0 + u * kXorThreads;
+                const uint64_t pos = base + ((uint64_t)w << 4);
+                v[k][u] = (w < words_per_unit && pos < a.in[k].valid) ? ld_cg(a.in[k].base + pos)
+                                                                       : make_uint4(0, 0, 0, 0);
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < kXorUnroll; ++u) {
+            acc[u] = v[0][u];
+#pragma unroll
+            for (int k = 1; k < NIN; ++k) {
+                acc[u].x ^= v[k][u].x;
+                acc[u].y ^= v[k][u].y;
+                acc[u].z ^= v[k][u].z;
+                acc[u].w ^= v[k][u].w;
+            }
+        }
+        const uint64_t obase = s * a.out_stride + a.out_off;
+#pragma unroll
+        for (int u = 0; u < kXorUnroll; ++u) {
+            const uint32_t w = w0 + u * kXorThreads;
+            const uint64_t pos = obase + ((uint64_t)w << 4);
+            if (w < words_per_unit && pos < a.out_valid) *reinterpret_cast<uint4 *>(a.out + pos) = acc[u];
+        }
+    }
+}
+
+template <int N>
+cudaError_t launch_xor_n(const XorArgs &a, int grid, cudaStream_t s) {
+    xor_kernel<N><<<grid, kXorThreads, 0, s>>>(a);
+    return cudaGetLastError();
+}
+
+}  // namespace
+
+cudaError_t launch_pack(const PackArgs &a, int grid, cudaStream_t s, bool tma) {
+    if (a.count == 0) return cudaSuccess;
+    if (tma) {
+        static bool attr_set = false;  // per process; the attribute is per function
+        const int smem = kTmaStages * kTmaStage;
+        if (!attr_set) {
+            cudaError_t e = cudaFuncSetAttribute(pack_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+            if (e != cudaSuccess) return e;
+            attr_set = true;
+        }
+        // 3 CTAs of 64 KiB SMEM per SM
+        uint64_t g = a.count < (uint64_t)grid * 3 / 2 ? a.count : (uint64_t)grid * 3 / 2;
+        pack_tma_kernel<<<(unsigned)g, kTmaThreads, smem, s>>>(a);
+        return cudaGetLastError();
+    }
+    uint64_t g = a.count < (uint64_t)grid ? a.count : (uint64_t)grid;
+    pack_kernel<<<(unsigned)g, kPackThreads, 0, s>>>(a);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_xor(const XorArgs &a, int max_ctas, cudaStream_t s) {
+    if (a.nstripes == 0 || a.nin < 1 || a.nin > kMaxTerms || (a.unit & 15)) return cudaErrorInvalidValue;
+    const uint64_t wpu = a.unit >> 4;
+    const uint64_t tpu = (wpu + kXorThreads * kXorUnroll - 1) / (kXorThreads * kXorUnroll);
+    uint64_t ntiles = a.nstripes * tpu;
+    int grid = (int)(ntiles < (uint64_t)max_ctas ? ntiles : (uint64_t)max_ctas);
+    switch (a.nin) {
+        case 1: return launch_xor_n<1>(a, grid, s);
+        case 2: return launch_xor_n<2>(a, grid, s);
+        case 3: return launch_xor_n<3>(a, grid, s);
+        case 4: return launch_xor_n<4>(a, grid, s);
+        case 5: return launch_xor_n<5>(a, grid, s);
+        case 6: return launch_xor_n<6>(a, grid, s);
+        case 7: return launch_xor_n<7>(a, grid, s);
+        default: return launch_xor_n<8>(a, grid, s);
+    }
+}
+
+}  // namespace reft

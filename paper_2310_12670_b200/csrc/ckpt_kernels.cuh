@@ -1,0 +1,62 @@
+// ckpt_kernels.cuh -- device-side data structures and launchers of libreft_ckpt.
+// Product code (the CUDA path); shares nothing with oracle/.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace reft {
+
+// One contiguous piece of the packed image: bytes [dst, dst + nbytes) of the image
+// come from device address src (src == 0: zero fill -- alignment gaps, reading Q6).
+// Built once by the planner at ckpt_register; sorted by dst.
+struct PackChunk {
+    uint64_t src;
+    uint64_t dst;
+    uint64_t nbytes;
+    uint64_t seg;
+};
+
+// Pack (tensors -> slot) or unpack (slot -> tensors) of the chunks [first, first+count)
+// clipped to the bucket's image range [bucket_begin, bucket_end).  The slot holds
+// image byte bucket_begin at address slot.
+struct PackArgs {
+    const PackChunk *chunks;
+    uint64_t first, count;
+    uint64_t bucket_begin, bucket_end;
+    uint8_t *slot;
+    int unpack;
+};
+
+// One input stream of an XOR-gather: for stripe s and word i of a unit, the input
+// byte address is base + s * stride + off + 16 * i; bytes at or beyond `valid`
+// (relative to base) read as zero (zero pad of ranks shorter than L*, reading Q5).
+struct XorTerm {
+    const uint8_t *base;
+    uint64_t valid;
+    uint64_t stride;
+    uint64_t off;
+};
+
+constexpr int kMaxTerms = 8;
+
+// out[s * out_stride + out_off + w] = XOR_t in_t[s * stride_t + off_t + w] for every
+// stripe s < nstripes and byte w < unit (unit a multiple of 16).  Writes at or
+// beyond out_valid are skipped.  Encode (Eq 1): terms = the m-1 peers' data slots,
+// out = own parity slot.  Rebuild (Eq 2): terms = own parity + the m-2 other
+// survivors, out = the lost rank's data slot (a P2P store over NVLink).
+struct XorArgs {
+    XorTerm in[kMaxTerms];
+    int nin;
+    uint8_t *out;
+    uint64_t out_valid;
+    uint64_t out_stride;
+    uint64_t out_off;
+    uint64_t nstripes;
+    uint64_t unit;
+};
+
+// Launchers (return the cudaError_t of the launch).
+cudaError_t launch_pack(const PackArgs &a, int grid, cudaStream_t s, bool tma);
+cudaError_t launch_xor(const XorArgs &a, int max_ctas, cudaStream_t s);
+
+}  // namespace reft

@@ -1,0 +1,1388 @@
+// ckpt_lib.cu -- host side of libreft_ckpt: C ABI, planner, pinned host arena, peer
+// mapping (CUDA IPC / in-process), and the bucket pipeline scheduler.
+//
+// Pipeline of one snapshot, per bucket k (slot s = k mod n_slots):
+//   stream P (pack)  : [slot reuse: own D2H(k-n) done, every peer's XOR(k-n) done]
+//                      pack(k) -> READY(k) to every peer
+//   stream X (xor)   : own pack(k), every peer's READY(k), [parity slot D2H(k-n)]
+//                      xor_encode(k) over NVLink -> REL(k) to every peer
+//   stream C (copy)  : D2H data slot(k) ; D2H parity slot(k)   (copy engine, no SMs)
+//   end              : DONE to every peer; ckpt_wait waits DONE from all, commits.
+// Cross-rank signals are 32-bit sequence numbers.  IPC groups write them into the
+// peers' flag pages with stream memory operations (cuStreamWriteValue32 /
+// cuStreamWaitValue32: zero SMs, no NCCL on the data path); LOCAL groups (all
+// members in this process) use CUDA events instead.
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <cudaTypedefs.h>
+
+#include <algorithm>
+#include <atomic>
+#include <cstdarg>
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include <sys/mman.h>
+#include <unistd.h>
+
+#include "../../include/ckpt.h"
+#include "ckpt_kernels.cuh"
+
+using namespace reft;
+
+// ------------------------------------------------------------------ errors ----------
+static thread_local std::string g_last_error;
+
+static int fail(int code, const char *fmt, ...) __attribute__((format(printf, 2, 3)));
+static int fail(int code, const char *fmt, ...) {
+    char buf[1024];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    g_last_error = buf;
+    return code;
+}
+
+#define CUDA_TRY(expr)                                                                          \
+    do {                                                                                        \
+        cudaError_t e_ = (expr);                                                                \
+        if (e_ != cudaSuccess)                                                                  \
+            return fail(CKPT_ECUDA, "%s: %s (%s:%d)", #expr, cudaGetErrorString(e_), __FILE__, \
+                        __LINE__);                                                              \
+    } while (0)
+
+// ------------------------------------------------------------------ driver memops ---
+static PFN_cuStreamWaitValue32_v8000 p_wait32 = nullptr;
+static PFN_cuStreamWriteValue32_v8000 p_write32 = nullptr;
+static std::once_flag g_memop_once;
+static int g_memop_status = CKPT_ECUDA;
+
+static int load_memops() {
+    std::call_once(g_memop_once, [] {
+        cudaDriverEntryPointQueryResult q1, q2;
+        void *f1 = nullptr, *f2 = nullptr;
+        if (cudaGetDriverEntryPoint("cuStreamWaitValue32", &f1, cudaEnableDefault, &q1) == cudaSuccess &&
+            cudaGetDriverEntryPoint("cuStreamWriteValue32", &f2, cudaEnableDefault, &q2) == cudaSuccess &&
+            q1 == cudaDriverEntryPointSuccess && q2 == cudaDriverEntryPointSuccess && f1 && f2) {
+            p_wait32 = (PFN_cuStreamWaitValue32_v8000)f1;
+            p_write32 = (PFN_cuStreamWriteValue32_v8000)f2;
+            g_memop_status = CKPT_OK;
+        }
+    });
+    return g_memop_status;
+}
+
+// ------------------------------------------------------------------ constants -------
+namespace {
+constexpr uint32_t kMagic = 0x52454654u;  // "REFT"
+constexpr uint32_t kAbiVersion = 1;
+constexpr uint64_t kChunk = 64 * 1024;  // pack work item (bytes of image)
+// flag page: 3 arrays of CKPT_MAX_GROUP uint32, each on its own 128-B line
+enum Stage { kReady = 0, kRel = 1, kDone = 2, kNumStages = 3 };
+constexpr uint64_t kFlagStride = 32;  // uint32 per stage line
+constexpr uint64_t kFlagBytes = 4096;
+
+struct HandleBlob {  // exported by ckpt_export_handle; fixed layout, <= CKPT_HANDLE_BYTES
+    uint32_t magic, version;
+    int32_t device;
+    int32_t pid;
+    uint64_t L;             // this rank's packed length L_j
+    uint64_t align, unit;   // options that must agree
+    uint64_t slot_bytes;    // ring slot capacity
+    uint32_t n_slots;       // 0 = full copy
+    uint32_t full_copy;
+    uint64_t staging_bytes;
+    char host[64];
+    cudaIpcMemHandle_t staging_h;
+    cudaIpcMemHandle_t flags_h;
+};
+static_assert(sizeof(HandleBlob) <= CKPT_HANDLE_BYTES, "blob too large");
+
+inline uint64_t align_up(uint64_t x, uint64_t a) { return a ? (x + a - 1) / a * a : x; }
+inline uint32_t sigma(uint32_t r, uint32_t j) { return r - (r > j ? 1u : 0u); }
+
+struct Segment {
+    uint64_t dev, nbytes, off;
+    uint32_t dtype, role, flags;
+    std::string name;
+};
+
+struct TimedLaunch {
+    cudaEvent_t a, b;
+    int kind;  // 0 pack 1 xor 2 unpack 3 rebuild
+};
+
+struct HostBuf {
+    uint8_t *p = nullptr;
+    uint64_t bytes = 0;
+    bool mmapped = false;
+};
+}  // namespace
+
+struct ckpt_ctx {
+    int device = -1;
+    ckpt_options opt{};
+    int sm_count = 148;
+    int max_ctas = 296;
+    int sticky = CKPT_OK;
+    std::string sticky_msg;
+
+    // registration / plan
+    bool registered = false;
+    std::vector<Segment> segs;
+    uint64_t L = 0;  // L_j
+    std::vector<PackChunk> chunks;
+    PackChunk *d_chunks = nullptr;
+    ckpt_layout layout{};
+
+    // device staging (exported)
+    bool full_copy = false;
+    uint32_t n_slots = 0;
+    uint64_t slot_bytes = 0;
+    uint8_t *staging = nullptr;
+    uint64_t staging_bytes = 0;
+    uint32_t *flags = nullptr;  // local flag page (device), written by peers
+
+    // group
+    bool grouped = false;  // ckpt_protect succeeded (m >= 2) or m == 1 arena set up
+    uint32_t m = 1, me = 0, transport = CKPT_GROUP_IPC;
+    uint64_t Lstar = 0, unit = 0;
+    uint64_t peer_L[CKPT_MAX_GROUP] = {};
+    uint8_t *peer_staging[CKPT_MAX_GROUP] = {};
+    uint32_t *peer_flags[CKPT_MAX_GROUP] = {};
+    bool peer_opened[CKPT_MAX_GROUP] = {};
+    ckpt_ctx *members[CKPT_MAX_GROUP] = {};
+
+    // parity (local, not exported)
+    uint8_t *parity = nullptr;
+    uint64_t parity_bytes = 0, parity_slot_bytes = 0;
+
+    // host arena
+    HostBuf hdata[2], hpar[2];
+    int nbuf = 2;
+    int completed = -1, ongoing = 0;
+    uint64_t completed_id = 0;
+
+    // streams / events
+    cudaStream_t sP = nullptr, sX = nullptr, sC = nullptr, sW = nullptr;
+    cudaEvent_t ev_capture = nullptr, ev_pack_all = nullptr, ev_done = nullptr, ev_t0 = nullptr,
+                ev_t1 = nullptr;
+    std::vector<cudaEvent_t> ev_packed, ev_xored, ev_d2h_data, ev_d2h_par, ev_h2d, ev_kdone;
+    // LOCAL transport: per-stage per-slot signal events
+    std::vector<cudaEvent_t> ev_sig[kNumStages];
+
+    // op state
+    uint32_t seq = 0;
+    uint64_t next_id = 1;
+    uint64_t pending_id = 0;   // issued snapshot not yet waited
+    bool requested = false;    // LOCAL: ckpt_snapshot called, group not yet issued
+    bool issued = false;
+    uint64_t req_bucket = 0;
+    uint64_t op_B = 0, op_NB = 0;
+    uint32_t op_seq_base = 0;
+    bool rebuild_requested = false;
+    int32_t rebuild_lost = -1;
+
+    // stats
+    ckpt_stats st{};
+    std::vector<TimedLaunch> timed;
+    size_t timed_used = 0;
+};
+
+// ------------------------------------------------------------------ small helpers ---
+static int set_dev(ckpt_ctx *c) {
+    CUDA_TRY(cudaSetDevice(c->device));
+    return CKPT_OK;
+}
+
+static int ensure_events(std::vector<cudaEvent_t> &v, size_t n) {
+    while (v.size() < n) {
+        cudaEvent_t e;
+        CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        v.push_back(e);
+    }
+    return CKPT_OK;
+}
+
+static void destroy_events(std::vector<cudaEvent_t> &v) {
+    for (auto e : v) cudaEventDestroy(e);
+    v.clear();
+}
+
+// Timed launch bracket (CKPT_OPT_TIMING): events on the launching stream.
+static int timed_begin(ckpt_ctx *c, cudaStream_t s, int kind, TimedLaunch **out) {
+    *out = nullptr;
+    if (!(c->opt.flags & CKPT_OPT_TIMING)) return CKPT_OK;
+    if (c->timed_used == c->timed.size()) {
+        TimedLaunch t;
+        CUDA_TRY(cudaEventCreate(&t.a));
+        CUDA_TRY(cudaEventCreate(&t.b));
+        c->timed.push_back(t);
+    }
+    TimedLaunch *t = &c->timed[c->timed_used++];
+    t->kind = kind;
+    CUDA_TRY(cudaEventRecord(t->a, s));
+    *out = t;
+    return CKPT_OK;
+}
+
+static int timed_end(TimedLaunch *t, cudaStream_t s) {
+    if (t) CUDA_TRY(cudaEventRecord(t->b, s));
+    return CKPT_OK;
+}
+
+static int harvest_timing(ckpt_ctx *c) {
+    for (size_t i = 0; i < c->timed_used; ++i) {
+        float ms = 0;
+        CUDA_TRY(cudaEventElapsedTime(&ms, c->timed[i].a, c->timed[i].b));
+        switch (c->timed[i].kind) {
+            case 0: c->st.pack_ms += ms; break;
+            case 1: c->st.xor_ms += ms; break;
+            case 2: c->st.unpack_ms += ms; break;
+            default: c->st.rebuild_ms += ms; break;
+        }
+    }
+    c->timed_used = 0;
+    return CKPT_OK;
+}
+
+// ------------------------------------------------------------------ host arena ------
+// Pinned host memory: anonymous mmap with transparent huge pages, pre-faulted by a few
+// threads, then cudaHostRegister (page-locked, device-mapped).  Falls back to
+// cudaHostAlloc.  Zero-filled (the pad of the image must read as zero, Q5).
+static int host_alloc(HostBuf &b, uint64_t bytes) {
+    b = HostBuf{};
+    if (bytes == 0) return CKPT_OK;
+    uint64_t len = align_up(bytes, 2ull << 20);
+    void *p = mmap(nullptr, len, PROT_READ | PROT_WRITE, MAP_PRIVATE | MAP_ANONYMOUS | MAP_NORESERVE, -1, 0);
+    if (p != MAP_FAILED) {
+#ifdef MADV_HUGEPAGE
+        madvise(p, len, MADV_HUGEPAGE);
+#endif
+        unsigned nt = std::min(16u, std::max(1u, std::thread::hardware_concurrency() / 2));
+        std::vector<std::thread> th;
+        const uint64_t per = align_up(len / nt + 1, 2ull << 20);
+        for (unsigned i = 0; i < nt; ++i)
+            th.emplace_back([=] {
+                uint8_t *q = (uint8_t *)p;
+                for (uint64_t o = i * per; o < std::min(len, (i + 1) * per); o += 4096) q[o] = 0;
+            });
+        for (auto &t : th) t.join();
+        if (cudaHostRegister(p, len, cudaHostRegisterPortable) == cudaSuccess) {
+            b.p = (uint8_t *)p;
+            b.bytes = len;
+            b.mmapped = true;
+            return CKPT_OK;
+        }
+        cudaGetLastError();
+        munmap(p, len);
+    }
+    void *q = nullptr;
+    if (cudaHostAlloc(&q, bytes, cudaHostAllocPortable) != cudaSuccess) {
+        cudaGetLastError();
+        return fail(CKPT_ENOMEM, "pinned host allocation of %llu bytes failed", (unsigned long long)bytes);
+    }
+    memset(q, 0, bytes);
+    b.p = (uint8_t *)q;
+    b.bytes = bytes;
+    return CKPT_OK;
+}
+
+static void host_free(HostBuf &b) {
+    if (!b.p) return;
+    if (b.mmapped) {
+        cudaHostUnregister(b.p);
+        munmap(b.p, b.bytes);
+    } else {
+        cudaFreeHost(b.p);
+    }
+    b = HostBuf{};
+}
+
+// ------------------------------------------------------------------ planner ---------
+extern "C" int ckpt_plan_layout(const uint64_t *nbytes, uint64_t n, uint32_t align, uint64_t *offsets,
+                                uint64_t *L) {
+    if (!L || (n && (!nbytes || !offsets)) || align == 0) return fail(CKPT_EINVAL, "plan_layout: bad args");
+    uint64_t end = 0;
+    for (uint64_t t = 0; t < n; ++t) {
+        offsets[t] = align_up(end, align);
+        end = offsets[t] + nbytes[t];
+    }
+    *L = align_up(end, align);
+    return CKPT_OK;
+}
+
+extern "C" int ckpt_plan_common(const uint64_t *Lj, uint32_t m, uint64_t unit, uint64_t *L_star,
+                                uint64_t *unit_eff) {
+    if (!Lj || !L_star || !unit_eff || m < 1 || m > CKPT_MAX_GROUP)
+        return fail(CKPT_EINVAL, "plan_common: bad args");
+    uint64_t mx = 0;
+    for (uint32_t j = 0; j < m; ++j) mx = std::max(mx, Lj[j]);
+    if (m == 1) {
+        *L_star = Lj[0];
+        *unit_eff = unit;
+    } else if (unit == 0) {  // SPEC S.378 whole-shard split: one stripe
+        *L_star = align_up(mx, (uint64_t)(m - 1) * 256);
+        *unit_eff = *L_star / (m - 1);
+    } else {
+        *L_star = align_up(mx, (uint64_t)(m - 1) * unit);
+        *unit_eff = unit;
+    }
+    return CKPT_OK;
+}
+
+// ------------------------------------------------------------------ lifecycle -------
+extern "C" void ckpt_options_default(ckpt_options *o) {
+    if (!o) return;
+    memset(o, 0, sizeof *o);
+    o->struct_size = sizeof(ckpt_options);
+    o->align = 256;
+    o->stripe_unit = 64 * 1024;
+    o->bucket_bytes = 64ull << 20;
+    o->n_slots = 4;
+    o->host_buffers = 2;
+    o->priority = INT32_MAX;  // resolved to the least priority at create
+    o->max_ctas = 0;
+    o->flags = 0;
+}
+
+extern "C" const char *ckpt_version(void) { return "reft-ckpt 0.1 sm_100a"; }
+
+extern "C" const char *ckpt_strerror(int code) {
+    switch (code) {
+        case CKPT_OK: return "ok";
+        case CKPT_EINVAL: return "invalid argument";
+        case CKPT_ECUDA: return "CUDA error";
+        case CKPT_ENOMEM: return "out of memory";
+        case CKPT_ESTATE: return "invalid state for this call";
+        case CKPT_EUNAVAIL: return "protection unavailable (group of one)";
+        case CKPT_EMISMATCH: return "group geometry mismatch";
+        case CKPT_EPEER: return "peer mapping failed";
+        case CKPT_EBUSY: return "previous snapshot not waited";
+        case CKPT_ENOSNAP: return "no completed snapshot";
+        case CKPT_EUNRECOVERABLE: return "unrecoverable: more losses than tolerated";
+        default: return "unknown error";
+    }
+}
+
+extern "C" const char *ckpt_last_error(void) { return g_last_error.c_str(); }
+
+extern "C" int ckpt_create(int device, const ckpt_options *o, ckpt_ctx **out) {
+    if (!out) return fail(CKPT_EINVAL, "create: out is NULL");
+    *out = nullptr;
+    ckpt_options opt;
+    ckpt_options_default(&opt);
+    if (o) {
+        if (o->struct_size != sizeof(ckpt_options)) return fail(CKPT_EINVAL, "create: struct_size mismatch");
+        opt = *o;
+    }
+    if (opt.align < 16 || opt.align > 4096 || (opt.align & (opt.align - 1)))
+        return fail(CKPT_EINVAL, "create: align must be a power of two in [16, 4096]");
+    if (opt.stripe_unit % 16) return fail(CKPT_EINVAL, "create: stripe_unit must be a multiple of 16");
+    if (opt.host_buffers != 1 && opt.host_buffers != 2) return fail(CKPT_EINVAL, "create: host_buffers must be 1 or 2");
+    if (opt.n_slots == 1) return fail(CKPT_EINVAL, "create: n_slots must be 0 (full copy) or >= 2");
+    if (opt.bucket_bytes < 4096) return fail(CKPT_EINVAL, "create: bucket_bytes must be >= 4096");
+    if ((opt.flags & CKPT_OPT_TMA_PACK) && (opt.flags & CKPT_OPT_LSU_PACK))
+        return fail(CKPT_EINVAL, "create: TMA_PACK and LSU_PACK are exclusive");
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
+        cudaGetLastError();
+        return fail(CKPT_ECUDA, "create: no CUDA device available (no CPU fallback)");
+    }
+    if (device < 0 || device >= ndev) return fail(CKPT_EINVAL, "create: device %d out of range", device);
+    ckpt_ctx *c = new ckpt_ctx();
+    c->device = device;
+    c->opt = opt;
+    c->nbuf = (int)opt.host_buffers;
+    int rc = set_dev(c);
+    if (rc) {
+        delete c;
+        return rc;
+    }
+    cudaDeviceGetAttribute(&c->sm_count, cudaDevAttrMultiProcessorCount, device);
+    c->max_ctas = opt.max_ctas ? (int)opt.max_ctas : 2 * c->sm_count;
+    int least = 0, greatest = 0;
+    cudaDeviceGetStreamPriorityRange(&least, &greatest);
+    int prio = opt.priority == INT32_MAX ? least : std::min(least, std::max(greatest, (int)opt.priority));
+    c->opt.priority = prio;
+    cudaError_t e = cudaSuccess;
+    cudaStream_t *ss[4] = {&c->sP, &c->sX, &c->sC, &c->sW};
+    for (auto s : ss)
+        if (e == cudaSuccess) e = cudaStreamCreateWithPriority(s, cudaStreamNonBlocking, prio);
+    cudaEvent_t *es[3] = {&c->ev_capture, &c->ev_pack_all, &c->ev_done};
+    for (auto ev : es)
+        if (e == cudaSuccess) e = cudaEventCreateWithFlags(ev, cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaEventCreate(&c->ev_t0);
+    if (e == cudaSuccess) e = cudaEventCreate(&c->ev_t1);
+    if (e != cudaSuccess) {
+        ckpt_destroy(c);
+        return fail(CKPT_ECUDA, "create: %s", cudaGetErrorString(e));
+    }
+    *out = c;
+    return CKPT_OK;
+}
+
+extern "C" int ckpt_destroy(ckpt_ctx *c) {
+    if (!c) return CKPT_OK;
+    cudaSetDevice(c->device);
+    cudaStream_t ss[4] = {c->sP, c->sX, c->sC, c->sW};
+    for (auto s : ss)
+        if (s) cudaStreamSynchronize(s);
+    for (uint32_t j = 0; j < CKPT_MAX_GROUP; ++j) {
+        if (c->peer_opened[j]) {
+            if (c->peer_staging[j]) cudaIpcCloseMemHandle(c->peer_staging[j]);
+            if (c->peer_flags[j]) cudaIpcCloseMemHandle(c->peer_flags[j]);
+        }
+    }
+    for (auto s : ss)
+        if (s) cudaStreamDestroy(s);
+    cudaEvent_t es[5] = {c->ev_capture, c->ev_pack_all, c->ev_done, c->ev_t0, c->ev_t1};
+    for (auto e : es)
+        if (e) cudaEventDestroy(e);
+    destroy_events(c->ev_packed);
+    destroy_events(c->ev_xored);
+    destroy_events(c->ev_d2h_data);
+    destroy_events(c->ev_d2h_par);
+    destroy_events(c->ev_h2d);
+    destroy_events(c->ev_kdone);
+    for (auto &v : c->ev_sig) destroy_events(v);
+    for (auto &t : c->timed) {
+        cudaEventDestroy(t.a);
+        cudaEventDestroy(t.b);
+    }
+    if (c->d_chunks) cudaFree(c->d_chunks);
+    if (c->staging) cudaFree(c->staging);
+    if (c->flags) cudaFree(c->flags);
+    if (c->parity) cudaFree(c->parity);
+    for (int i = 0; i < 2; ++i) {
+        host_free(c->hdata[i]);
+        host_free(c->hpar[i]);
+    }
+    cudaGetLastError();
+    delete c;
+    return CKPT_OK;
+}
+
+// ------------------------------------------------------------------ register --------
+extern "C" int ckpt_register(ckpt_ctx *c, const ckpt_tensor *t, uint64_t n, const ckpt_layout *layout) {
+    if (!c || !t || n == 0) return fail(CKPT_EINVAL, "register: null context/tensors or n == 0");
+    if (c->registered) return fail(CKPT_ESTATE, "register: already registered");
+    int rc = set_dev(c);
+    if (rc) return rc;
+    std::vector<Segment> segs(n);
+    for (uint64_t i = 0; i < n; ++i) {
+        if (!t[i].dev_ptr || t[i].nbytes == 0) return fail(CKPT_EINVAL, "register: tensor %llu null or empty", (unsigned long long)i);
+        cudaPointerAttributes pa;
+        if (cudaPointerGetAttributes(&pa, t[i].dev_ptr) != cudaSuccess || pa.type != cudaMemoryTypeDevice ||
+            pa.device != c->device) {
+            cudaGetLastError();
+            return fail(CKPT_EINVAL, "register: tensor %llu is not device memory on device %d", (unsigned long long)i, c->device);
+        }
+        segs[i] = Segment{(uint64_t)(uintptr_t)t[i].dev_ptr, t[i].nbytes, 0, t[i].dtype, t[i].role, t[i].flags,
+                          t[i].name ? t[i].name : ""};
+    }
+    // plan (reading Q6): registration order, A-aligned offsets, zero gaps
+    uint64_t end = 0;
+    std::vector<PackChunk> ch;
+    for (uint64_t i = 0; i < n; ++i) {
+        uint64_t off = align_up(end, c->opt.align);
+        if (off > end) ch.push_back(PackChunk{0, end, off - end, i});  // zero gap
+        segs[i].off = off;
+        for (uint64_t o = 0; o < segs[i].nbytes;) {
+            // cut at image offsets that are multiples of kChunk so buckets split cleanly
+            uint64_t img = off + o;
+            uint64_t lim = std::min(segs[i].nbytes - o, align_up(img + 1, kChunk) - img);
+            ch.push_back(PackChunk{segs[i].dev + o, img, lim, i});
+            o += lim;
+        }
+        end = off + segs[i].nbytes;
+    }
+    uint64_t L = align_up(end, c->opt.align);
+    if (L > end) ch.push_back(PackChunk{0, end, L - end, n});
+    // device staging: full image (n_slots == 0) or a ring of n_slots buckets
+    c->full_copy = c->opt.n_slots == 0;
+    c->n_slots = c->opt.n_slots;
+    c->slot_bytes = align_up(c->opt.bucket_bytes, 4096);
+    c->staging_bytes = c->full_copy ? std::max<uint64_t>(L, 4096) : (uint64_t)c->n_slots * c->slot_bytes;
+    PackChunk *dch = nullptr;
+    if (cudaMalloc(&dch, ch.size() * sizeof(PackChunk)) != cudaSuccess) {
+        cudaGetLastError();
+        return fail(CKPT_ENOMEM, "register: chunk table allocation failed");
+    }
+    CUDA_TRY(cudaMemcpy(dch, ch.data(), ch.size() * sizeof(PackChunk), cudaMemcpyHostToDevice));
+    if (cudaMalloc(&c->staging, c->staging_bytes) != cudaSuccess ||
+        cudaMalloc(&c->flags, kFlagBytes) != cudaSuccess) {
+        cudaGetLastError();
+        cudaFree(dch);
+        if (c->staging) cudaFree(c->staging);
+        c->staging = nullptr;
+        return fail(CKPT_ENOMEM, "register: device staging of %llu bytes failed", (unsigned long long)c->staging_bytes);
+    }
+    CUDA_TRY(cudaMemset(c->flags, 0, kFlagBytes));
+    CUDA_TRY(cudaMemset(c->staging, 0, c->staging_bytes));
+    c->d_chunks = dch;
+    c->chunks = std::move(ch);
+    c->segs = std::move(segs);
+    c->L = L;
+    if (layout) c->layout = *layout;
+    c->registered = true;
+    return CKPT_OK;
+}
+
+extern "C" int ckpt_geometry(const ckpt_ctx *c, uint64_t *Ll, uint64_t *Ls, uint64_t *u, uint32_t *m) {
+    if (!c) return fail(CKPT_EINVAL, "geometry: null context");
+    if (!c->registered) return fail(CKPT_ESTATE, "geometry: not registered");
+    if (Ll) *Ll = c->L;
+    if (Ls) *Ls = c->grouped ? c->Lstar : c->L;
+    if (u) *u = c->grouped ? c->unit : c->opt.stripe_unit;
+    if (m) *m = c->m;
+    return CKPT_OK;
+}
+
+extern "C" int ckpt_tensor_offset(const ckpt_ctx *c, uint64_t t, uint64_t *off) {
+    if (!c || !off) return fail(CKPT_EINVAL, "tensor_offset: null");
+    if (!c->registered || t >= c->segs.size()) return fail(CKPT_EINVAL, "tensor_offset: bad index");
+    *off = c->segs[t].off;
+    return CKPT_OK;
+}
+
+// ------------------------------------------------------------------ group -----------
+extern "C" int ckpt_export_handle(ckpt_ctx *c, void *buf, uint64_t *len) {
+    if (!c || !buf || !len || *len < CKPT_HANDLE_BYTES) return fail(CKPT_EINVAL, "export_handle: bad args");
+    if (!c->registered) return fail(CKPT_ESTATE, "export_handle: not registered");
+    int rc = set_dev(c);
+    if (rc) return rc;
+    HandleBlob b;
+    memset(&b, 0, sizeof b);
+    b.magic = kMagic;
+    b.version = kAbiVersion;
+    b.device = c->device;
+    b.pid = (int32_t)getpid();
+    b.L = c->L;
+    b.align = c->opt.align;
+    b.unit = c->opt.stripe_unit;
+    b.slot_bytes = c->slot_bytes;
+    b.n_slots = c->n_slots;
+    b.full_copy = c->full_copy;
+    b.staging_bytes = c->staging_bytes;
+    gethostname(b.host, sizeof b.host - 1);
+    CUDA_TRY(cudaIpcGetMemHandle(&b.staging_h, c->staging));
+    CUDA_TRY(cudaIpcGetMemHandle(&b.flags_h, c->flags));
+    memset(buf, 0, CKPT_HANDLE_BYTES);
+    memcpy(buf, &b, sizeof b);
+    *len = CKPT_HANDLE_BYTES;
+    return CKPT_OK;
+}
+
+static int alloc_arena(ckpt_ctx *c) {
+    const uint64_t pbytes = c->m >= 2 ? c->Lstar / (c->m - 1) : 0;
+    for (int i = 0; i < c->nbuf; ++i) {
+        int rc = host_alloc(c->hdata[i], c->Lstar);
+        if (!rc && pbytes) rc = host_alloc(c->hpar[i], pbytes);
+        if (rc) {
+            for (int k = 0; k < 2; ++k) {
+                host_free(c->hdata[k]);
+                host_free(c->hpar[k]);
+            }
+            return rc;
+        }
+    }
+    c->completed = -1;
+    c->ongoing = 0;
+    return CKPT_OK;
+}
+
+static int setup_ungrouped(ckpt_ctx *c) {
+    c->m = 1;
+    c->me = 0;
+    c->Lstar = c->L;
+    c->unit = c->opt.stripe_unit;
+    c->peer_L[0] = c->L;
+    c->peer_staging[0] = c->staging;
+    c->members[0] = c;
+    int rc = alloc_arena(c);
+    if (rc) return rc;
+    c->grouped = true;
+    return CKPT_OK;
+}
+
+extern "C" int ckpt_protect(ckpt_ctx *c, const ckpt_group *g) {
+    if (!c || !g) return fail(CKPT_EINVAL, "protect: null");
+    if (!c->registered) return fail(CKPT_ESTATE, "protect: not registered");
+    if (c->grouped) return fail(CKPT_ESTATE, "protect: group already bound");
+    if (g->m < 1 || g->m > CKPT_MAX_GROUP || g->my_index >= g->m)
+        return fail(CKPT_EINVAL, "protect: m must be in [1, %u] and my_index < m", CKPT_MAX_GROUP);
+    int rc = set_dev(c);
+    if (rc) return rc;
+    if (g->m == 1) {
+        rc = setup_ungrouped(c);
+        return rc ? rc : fail(CKPT_EUNAVAIL, "protect: a group of one has no redundancy (SPEC S.314)");
+    }
+    const uint32_t m = g->m;
+    uint64_t Ls[CKPT_MAX_GROUP];
+    if (g->transport == CKPT_GROUP_IPC) {
+        if (!g->handles) return fail(CKPT_EINVAL, "protect: IPC group without handles");
+        if (load_memops()) return fail(CKPT_ECUDA, "protect: stream memory operations unavailable");
+        const HandleBlob *hb[CKPT_MAX_GROUP];
+        for (uint32_t j = 0; j < m; ++j) {
+            hb[j] = (const HandleBlob *)((const uint8_t *)g->handles + (uint64_t)j * CKPT_HANDLE_BYTES);
+            if (hb[j]->magic != kMagic || hb[j]->version != kAbiVersion)
+                return fail(CKPT_EINVAL, "protect: handle %u is not a reft-ckpt v%u blob", j, kAbiVersion);
+            if (hb[j]->align != c->opt.align || hb[j]->unit != c->opt.stripe_unit ||
+                hb[j]->slot_bytes != c->slot_bytes || hb[j]->n_slots != c->n_slots || hb[j]->full_copy != (uint32_t)c->full_copy)
+                return fail(CKPT_EMISMATCH, "protect: member %u geometry differs (align/unit/slots)", j);
+            if (strncmp(hb[j]->host, hb[g->my_index]->host, sizeof hb[j]->host) != 0)
+                return fail(CKPT_EMISMATCH, "protect: member %u is on another host (node group only, Q1)", j);
+            Ls[j] = hb[j]->L;
+        }
+        if (hb[g->my_index]->pid != (int32_t)getpid() || hb[g->my_index]->L != c->L)
+            return fail(CKPT_EINVAL, "protect: my_index does not point at this context's handle");
+        for (uint32_t j = 0; j < m; ++j) {
+            c->peer_L[j] = Ls[j];
+            if (j == g->my_index) {
+                c->peer_staging[j] = c->staging;
+                c->peer_flags[j] = c->flags;
+                continue;
+            }
+            void *ps = nullptr, *pf = nullptr;
+            cudaError_t e1 = cudaIpcOpenMemHandle(&ps, hb[j]->staging_h, cudaIpcMemLazyEnablePeerAccess);
+            cudaError_t e2 = e1 == cudaSuccess ? cudaIpcOpenMemHandle(&pf, hb[j]->flags_h, cudaIpcMemLazyEnablePeerAccess)
+                                               : e1;
+            if (e1 != cudaSuccess || e2 != cudaSuccess) {
+                cudaGetLastError();
+                if (ps) cudaIpcCloseMemHandle(ps);
+                for (uint32_t k = 0; k < j; ++k)
+                    if (c->peer_opened[k]) {
+                        cudaIpcCloseMemHandle(c->peer_staging[k]);
+                        cudaIpcCloseMemHandle(c->peer_flags[k]);
+                        c->peer_opened[k] = false;
+                    }
+                return fail(CKPT_EPEER, "protect: cudaIpcOpenMemHandle of member %u failed: %s", j,
+                            cudaGetErrorString(e1 != cudaSuccess ? e1 : e2));
+            }
+            c->peer_staging[j] = (uint8_t *)ps;
+            c->peer_flags[j] = (uint32_t *)pf;
+            c->peer_opened[j] = true;
+        }
+    } else if (g->transport == CKPT_GROUP_LOCAL) {
+        if (!g->members) return fail(CKPT_EINVAL, "protect: LOCAL group without members");
+        if (g->members[g->my_index] != c) return fail(CKPT_EINVAL, "protect: members[my_index] is not this context");
+        for (uint32_t j = 0; j < m; ++j) {
+            ckpt_ctx *o = g->members[j];
+            if (!o || !o->registered) return fail(CKPT_ESTATE, "protect: member %u not registered", j);
+            if (o->opt.align != c->opt.align || o->opt.stripe_unit != c->opt.stripe_unit ||
+                o->slot_bytes != c->slot_bytes || o->n_slots != c->n_slots || o->full_copy != c->full_copy)
+                return fail(CKPT_EMISMATCH, "protect: member %u geometry differs", j);
+            if (o->device != c->device) {
+                int can = 0;
+                cudaDeviceCanAccessPeer(&can, c->device, o->device);
+                if (!can) return fail(CKPT_EPEER, "protect: device %d cannot access device %d", c->device, o->device);
+                cudaError_t e = cudaDeviceEnablePeerAccess(o->device, 0);
+                if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled)
+                    return fail(CKPT_EPEER, "protect: enable peer access: %s", cudaGetErrorString(e));
+                cudaGetLastError();
+            }
+            Ls[j] = o->L;
+            c->peer_L[j] = o->L;
+            c->peer_staging[j] = o->staging;
+            c->members[j] = o;
+        }
+    } else {
+        return fail(CKPT_EINVAL, "protect: unknown transport %u", g->transport);
+    }
+    uint64_t Lstar = 0, ue = 0;
+    rc = ckpt_plan_common(Ls, m, c->opt.stripe_unit, &Lstar, &ue);
+    if (rc) return rc;
+    const uint64_t stripe = (uint64_t)(m - 1) * ue;
+    if (!c->full_copy && stripe > c->slot_bytes)
+        return fail(CKPT_EINVAL, "protect: stripe of %llu bytes exceeds ring slot capacity %llu (use n_slots=0 or a smaller unit)",
+                    (unsigned long long)stripe, (unsigned long long)c->slot_bytes);
+    c->m = m;
+    c->me = g->my_index;
+    c->transport = g->transport;
+    c->Lstar = Lstar;
+    c->unit = ue;
+    // parity buffer (local)
+    if (c->full_copy) {
+        c->parity_slot_bytes = 0;
+        c->parity_bytes = std::max<uint64_t>(Lstar / (m - 1), 4096);
+    } else {
+        c->parity_slot_bytes = (c->slot_bytes / stripe) * ue;
+        c->parity_bytes = c->parity_slot_bytes * c->n_slots;
+    }
+    if (cudaMalloc(&c->parity, c->parity_bytes) != cudaSuccess) {
+        cudaGetLastError();
+        return fail(CKPT_ENOMEM, "protect: parity buffer of %llu bytes failed", (unsigned long long)c->parity_bytes);
+    }
+    rc = alloc_arena(c);
+    if (rc) return rc;
+    c->seq = 0;
+    c->grouped = true;
+    return CKPT_OK;
+}
+
+// ------------------------------------------------------------------ geometry helpers
+static inline uint64_t bucket_begin(const ckpt_ctx *c, uint64_t k) { return k * c->op_B; }
+static inline uint64_t bucket_end(const ckpt_ctx *c, uint64_t k) { return std::min((k + 1) * c->op_B, c->Lstar); }
+static inline uint64_t valid_in_bucket(uint64_t Lj, uint64_t bb, uint64_t be) {
+    return Lj <= bb ? 0 : std::min(Lj, be) - bb;
+}
+static inline uint32_t slot_of(const ckpt_ctx *c, uint64_t k) { return c->full_copy ? (uint32_t)k : (uint32_t)(k % c->n_slots); }
+static inline uint8_t *slot_ptr(const ckpt_ctx *c, uint8_t *base, uint64_t k) {
+    return c->full_copy ? base + bucket_begin(c, k) : base + (uint64_t)(k % c->n_slots) * c->slot_bytes;
+}
+static inline uint8_t *parity_slot_ptr(const ckpt_ctx *c, uint64_t k) {
+    return c->full_copy ? c->parity + bucket_begin(c, k) / (c->m - 1)
+                        : c->parity + (uint64_t)(k % c->n_slots) * c->parity_slot_bytes;
+}
+static inline uint32_t bucket_seq(const ckpt_ctx *c, uint64_t k) { return c->op_seq_base + (uint32_t)k + 1; }
+static inline bool ring_reuse(const ckpt_ctx *c, uint64_t k) { return !c->full_copy && k >= c->n_slots; }
+
+// ------------------------------------------------------------------ signals ---------
+// signal(stage, seq): tell every other member that this member reached `seq`.
+static int sig_signal(ckpt_ctx *c, cudaStream_t s, int stage, uint32_t seq, uint32_t slot) {
+    if (c->m < 2) return CKPT_OK;
+    if (c->transport == CKPT_GROUP_IPC) {
+        for (uint32_t j = 0; j < c->m; ++j) {
+            if (j == c->me) continue;
+            CUdeviceptr a = (CUdeviceptr)(uintptr_t)(c->peer_flags[j] + stage * kFlagStride + c->me);
+            CUresult r = p_write32((CUstream)s, a, seq, CU_STREAM_WRITE_VALUE_DEFAULT);
+            if (r != CUDA_SUCCESS) return fail(CKPT_ECUDA, "cuStreamWriteValue32 failed (%d)", (int)r);
+        }
+        return CKPT_OK;
+    }
+    int rc = ensure_events(c->ev_sig[stage], slot + 1);
+    if (rc) return rc;
+    CUDA_TRY(cudaEventRecord(c->ev_sig[stage][slot], s));
+    return CKPT_OK;
+}
+
+// wait(stage, seq): stream s waits until member j signalled >= seq.
+static int sig_wait(ckpt_ctx *c, cudaStream_t s, uint32_t j, int stage, uint32_t seq, uint32_t slot) {
+    if (c->transport == CKPT_GROUP_IPC) {
+        CUdeviceptr a = (CUdeviceptr)(uintptr_t)(c->flags + stage * kFlagStride + j);
+        CUresult r = p_wait32((CUstream)s, a, seq, CU_STREAM_WAIT_VALUE_GEQ);
+        if (r != CUDA_SUCCESS) return fail(CKPT_ECUDA, "cuStreamWaitValue32 failed (%d)", (int)r);
+        return CKPT_OK;
+    }
+    ckpt_ctx *o = c->members[j];
+    if (o->ev_sig[stage].size() <= slot) return fail(CKPT_ESTATE, "internal: LOCAL wait before signal");
+    CUDA_TRY(cudaStreamWaitEvent(s, o->ev_sig[stage][slot], 0));
+    return CKPT_OK;
+}
+
+static int wait_all(ckpt_ctx *c, cudaStream_t s, int stage, uint32_t seq, uint32_t slot, int32_t skip = -1) {
+    for (uint32_t j = 0; j < c->m; ++j) {
+        if (j == c->me || (int32_t)j == skip) continue;
+        int rc = sig_wait(c, s, j, stage, seq, slot);
+        if (rc) return rc;
+    }
+    return CKPT_OK;
+}
+
+// ------------------------------------------------------------------ kernels ---------
+static int do_pack(ckpt_ctx *c, uint64_t k, uint8_t *slot, cudaStream_t s, bool unpack) {
+    const uint64_t bb = bucket_begin(c, k), be = std::min(bucket_end(c, k), c->L);
+    if (be <= bb) return CKPT_OK;
+    // chunk range overlapping [bb, be): chunks sorted by dst and contiguous
+    auto lo = std::upper_bound(c->chunks.begin(), c->chunks.end(), bb,
+                               [](uint64_t v, const PackChunk &x) { return v < x.dst + x.nbytes; });
+    auto hi = std::lower_bound(lo, c->chunks.end(), be, [](const PackChunk &x, uint64_t v) { return x.dst < v; });
+    PackArgs a;
+    a.chunks = c->d_chunks;
+    a.first = (uint64_t)(lo - c->chunks.begin());
+    a.count = (uint64_t)(hi - lo);
+    a.bucket_begin = bb;
+    a.bucket_end = be;
+    a.slot = slot;
+    a.unpack = unpack ? 1 : 0;
+    TimedLaunch *t;
+    int rc = timed_begin(c, s, unpack ? 2 : 0, &t);
+    if (rc) return rc;
+    CUDA_TRY(launch_pack(a, c->max_ctas, s, (c->opt.flags & CKPT_OPT_TMA_PACK) != 0));
+    rc = timed_end(t, s);
+    if (rc) return rc;
+    if (unpack) {
+        c->st.unpack_launches++;
+    } else {
+        c->st.pack_launches++;
+        c->st.pack_bytes += 2 * (be - bb);
+    }
+    return CKPT_OK;
+}
+
+// Encode row r = c->me for bucket k (Eq 1): terms are every peer j's data slot.
+static int do_encode(ckpt_ctx *c, uint64_t k, cudaStream_t s) {
+    const uint64_t bb = bucket_begin(c, k), be = bucket_end(c, k);
+    const uint64_t stripe = (uint64_t)(c->m - 1) * c->unit;
+    XorArgs a;
+    memset(&a, 0, sizeof a);
+    a.nin = 0;
+    uint64_t in_bytes = 0;
+    for (uint32_t j = 0; j < c->m; ++j) {
+        if (j == c->me) continue;
+        XorTerm &t = a.in[a.nin++];
+        t.base = slot_ptr(c, c->peer_staging[j], k);
+        t.valid = valid_in_bucket(c->peer_L[j], bb, be);
+        t.stride = stripe;
+        t.off = (uint64_t)sigma(c->me, j) * c->unit;
+        in_bytes += (be - bb) / (c->m - 1);
+    }
+    a.out = parity_slot_ptr(c, k);
+    a.out_valid = UINT64_MAX;
+    a.out_stride = c->unit;
+    a.out_off = 0;
+    a.nstripes = (be - bb) / stripe;
+    a.unit = c->unit;
+    TimedLaunch *t;
+    int rc = timed_begin(c, s, 1, &t);
+    if (rc) return rc;
+    CUDA_TRY(launch_xor(a, c->max_ctas, s));
+    rc = timed_end(t, s);
+    if (rc) return rc;
+    c->st.xor_launches++;
+    c->st.xor_bytes_in += in_bytes;
+    c->st.xor_bytes_out += (be - bb) / (c->m - 1);
+    return CKPT_OK;
+}
+
+// Rebuild row r = c->me (a survivor) of bucket k into lost rank kl's slot (Eq 2).
+static int do_rebuild_row(ckpt_ctx *c, uint64_t k, uint32_t kl, cudaStream_t s) {
+    const uint64_t bb = bucket_begin(c, k), be = bucket_end(c, k);
+    const uint64_t stripe = (uint64_t)(c->m - 1) * c->unit;
+    XorArgs a;
+    memset(&a, 0, sizeof a);
+    XorTerm &p = a.in[a.nin++];
+    p.base = parity_slot_ptr(c, k);
+    p.valid = UINT64_MAX;
+    p.stride = c->unit;
+    p.off = 0;
+    for (uint32_t j = 0; j < c->m; ++j) {
+        if (j == c->me || j == kl) continue;
+        XorTerm &t = a.in[a.nin++];
+        t.base = slot_ptr(c, c->peer_staging[j], k);
+        t.valid = valid_in_bucket(c->peer_L[j], bb, be);
+        t.stride = stripe;
+        t.off = (uint64_t)sigma(c->me, j) * c->unit;
+    }
+    a.out = slot_ptr(c, c->peer_staging[kl], k);
+    a.out_valid = valid_in_bucket(c->peer_L[kl], bb, be);
+    a.out_stride = stripe;
+    a.out_off = (uint64_t)sigma(c->me, kl) * c->unit;
+    a.nstripes = (be - bb) / stripe;
+    a.unit = c->unit;
+    TimedLaunch *t;
+    int rc = timed_begin(c, s, 3, &t);
+    if (rc) return rc;
+    CUDA_TRY(launch_xor(a, c->max_ctas, s));
+    rc = timed_end(t, s);
+    if (rc) return rc;
+    c->st.rebuild_launches++;
+    return CKPT_OK;
+}
+
+// ------------------------------------------------------------------ snapshot --------
+static int check_sticky(ckpt_ctx *c) {
+    if (c->sticky) return fail(c->sticky, "context has a sticky error: %s", c->sticky_msg.c_str());
+    return CKPT_OK;
+}
+
+static void make_sticky(ckpt_ctx *c, int rc) {
+    if (!c->sticky) {
+        c->sticky = rc;
+        c->sticky_msg = g_last_error;
+    }
+}
+
+static uint64_t effective_bucket(const ckpt_ctx *c, uint64_t req) {
+    uint64_t B = req ? req : c->opt.bucket_bytes;
+    if (c->m >= 2) {
+        const uint64_t stripe = (uint64_t)(c->m - 1) * c->unit;
+        B = std::max<uint64_t>(stripe, B / stripe * stripe);
+    } else {
+        B = std::max<uint64_t>(c->opt.align, B / c->opt.align * c->opt.align);
+    }
+    return B;
+}
+
+static int prepare_op(ckpt_ctx *c, uint64_t B) {
+    c->op_B = B;
+    c->op_NB = c->Lstar ? (c->Lstar + B - 1) / B : 0;
+    c->op_seq_base = c->seq;
+    c->seq += (uint32_t)c->op_NB + 1;
+    const size_t ne = c->full_copy ? (size_t)std::max<uint64_t>(c->op_NB, 1) : c->n_slots;
+    int rc = 0;
+    for (auto *v : {&c->ev_packed, &c->ev_xored, &c->ev_d2h_data, &c->ev_d2h_par, &c->ev_h2d, &c->ev_kdone})
+        if (!rc) rc = ensure_events(*v, ne);
+    return rc;
+}
+
+// Stage 1 of bucket k on member c: pack into its slot, then READY.
+static int stage_pack(ckpt_ctx *c, uint64_t k) {
+    const uint32_t s = slot_of(c, k);
+    int rc;
+    if (ring_reuse(c, k)) {
+        CUDA_TRY(cudaStreamWaitEvent(c->sP, c->ev_d2h_data[s], 0));
+        if (c->m >= 2 && (rc = wait_all(c, c->sP, kRel, bucket_seq(c, k - c->n_slots), s))) return rc;
+    }
+    if ((rc = do_pack(c, k, slot_ptr(c, c->staging, k), c->sP, false))) return rc;
+    CUDA_TRY(cudaEventRecord(c->ev_packed[s], c->sP));
+    if (c->m >= 2 && (rc = sig_signal(c, c->sP, kReady, bucket_seq(c, k), s))) return rc;
+    return CKPT_OK;
+}
+
+// Stage 2: parity of bucket k once every member's pack(k) is visible, then REL.
+static int stage_xor(ckpt_ctx *c, uint64_t k) {
+    if (c->m < 2) return CKPT_OK;
+    const uint32_t s = slot_of(c, k);
+    int rc;
+    CUDA_TRY(cudaStreamWaitEvent(c->sX, c->ev_packed[s], 0));
+    if ((rc = wait_all(c, c->sX, kReady, bucket_seq(c, k), s))) return rc;
+    if (ring_reuse(c, k)) CUDA_TRY(cudaStreamWaitEvent(c->sX, c->ev_d2h_par[s], 0));
+    if ((rc = do_encode(c, k, c->sX))) return rc;
+    CUDA_TRY(cudaEventRecord(c->ev_xored[s], c->sX));
+    return sig_signal(c, c->sX, kRel, bucket_seq(c, k), s);
+}
+
+// Stage 3: copy-engine D2H of data and parity into the ongoing host image.
+static int stage_copy(ckpt_ctx *c, uint64_t k) {
+    const uint32_t s = slot_of(c, k);
+    const uint64_t bb = bucket_begin(c, k), be = bucket_end(c, k);
+    const uint64_t v = valid_in_bucket(c->L, bb, be);
+    CUDA_TRY(cudaStreamWaitEvent(c->sC, c->ev_packed[s], 0));
+    if (v) {
+        CUDA_TRY(cudaMemcpyAsync(c->hdata[c->ongoing].p + bb, slot_ptr(c, c->staging, k), v, cudaMemcpyDeviceToHost, c->sC));
+        c->st.d2h_bytes += v;
+    }
+    CUDA_TRY(cudaEventRecord(c->ev_d2h_data[s], c->sC));
+    if (c->m >= 2) {
+        const uint64_t pb = (be - bb) / (c->m - 1);
+        CUDA_TRY(cudaStreamWaitEvent(c->sC, c->ev_xored[s], 0));
+        CUDA_TRY(cudaMemcpyAsync(c->hpar[c->ongoing].p + bb / (c->m - 1), parity_slot_ptr(c, k), pb,
+                                 cudaMemcpyDeviceToHost, c->sC));
+        c->st.d2h_bytes += pb;
+        CUDA_TRY(cudaEventRecord(c->ev_d2h_par[s], c->sC));
+    }
+    return CKPT_OK;
+}
+
+static int stage_finish(ckpt_ctx *c) {
+    CUDA_TRY(cudaEventRecord(c->ev_pack_all, c->sP));
+    CUDA_TRY(cudaStreamWaitEvent(c->sC, c->ev_pack_all, 0));
+    if (c->m >= 2) CUDA_TRY(cudaStreamWaitEvent(c->sC, c->ev_xored[slot_of(c, c->op_NB ? c->op_NB - 1 : 0)], 0));
+    CUDA_TRY(cudaEventRecord(c->ev_done, c->sC));
+    if (c->opt.flags & CKPT_OPT_TIMING) CUDA_TRY(cudaEventRecord(c->ev_t1, c->sC));
+    if (c->m >= 2) return sig_signal(c, c->sC, kDone, c->op_seq_base + (uint32_t)c->op_NB + 1, 0);
+    return CKPT_OK;
+}
+
+static int begin_member(ckpt_ctx *c, cudaStream_t caller, uint64_t B) {
+    int rc = prepare_op(c, B);
+    if (rc) return rc;
+    if (c->nbuf == 1) c->completed = -1;  // single buffer: overwritten in place
+    CUDA_TRY(cudaEventRecord(c->ev_capture, caller));
+    if (c->opt.flags & CKPT_OPT_TIMING) CUDA_TRY(cudaEventRecord(c->ev_t0, caller));
+    CUDA_TRY(cudaStreamWaitEvent(c->sP, c->ev_capture, 0));
+    return CKPT_OK;
+}
+
+extern "C" int ckpt_snapshot(ckpt_ctx *c, uint64_t bucket_bytes, void *stream, uint64_t *id) {
+    if (!c) return fail(CKPT_EINVAL, "snapshot: null context");
+    if (!c->registered) return fail(CKPT_ESTATE, "snapshot: not registered");
+    int rc = check_sticky(c);
+    if (rc) return rc;
+    if (c->pending_id || c->requested) return fail(CKPT_EBUSY, "snapshot: previous snapshot %llu not waited", (unsigned long long)c->pending_id);
+    if ((rc = set_dev(c))) return rc;
+    if (!c->grouped && (rc = setup_ungrouped(c))) return rc;
+    const uint64_t B = effective_bucket(c, bucket_bytes);
+    if (!c->full_copy && B > c->slot_bytes)
+        return fail(CKPT_EINVAL, "snapshot: bucket of %llu bytes exceeds slot capacity %llu", (unsigned long long)B,
+                    (unsigned long long)c->slot_bytes);
+    cudaStream_t caller = (cudaStream_t)stream;
+    const uint64_t my_id = c->next_id++;
+    if (c->m >= 2 && c->transport == CKPT_GROUP_LOCAL) {
+        c->req_bucket = B;
+        c->requested = true;
+        c->pending_id = my_id;
+        CUDA_TRY(cudaEventRecord(c->ev_capture, caller));  // capture point of this member
+        bool all = true;
+        for (uint32_t j = 0; j < c->m; ++j) all = all && c->members[j]->requested;
+        if (all) {
+            for (uint32_t j = 0; j < c->m; ++j)
+                if (c->members[j]->req_bucket != B) return fail(CKPT_EINVAL, "snapshot: members passed different bucket sizes");
+            // keep each member's capture event: begin_member must not re-record it
+            for (uint32_t j = 0; j < c->m; ++j) {
+                ckpt_ctx *o = c->members[j];
+                if ((rc = set_dev(o)) || (rc = prepare_op(o, B))) return rc;
+                if (o->nbuf == 1) o->completed = -1;
+                CUDA_TRY(cudaStreamWaitEvent(o->sP, o->ev_capture, 0));
+                if (o->opt.flags & CKPT_OPT_TIMING) CUDA_TRY(cudaEventRecord(o->ev_t0, o->sP));
+            }
+            for (uint64_t k = 0; k < c->op_NB; ++k) {
+                for (uint32_t j = 0; j < c->m; ++j)
+                    if ((rc = set_dev(c->members[j])) || (rc = stage_pack(c->members[j], k))) goto bad;
+                for (uint32_t j = 0; j < c->m; ++j)
+                    if ((rc = set_dev(c->members[j])) || (rc = stage_xor(c->members[j], k))) goto bad;
+                for (uint32_t j = 0; j < c->m; ++j)
+                    if ((rc = set_dev(c->members[j])) || (rc = stage_copy(c->members[j], k))) goto bad;
+            }
+            for (uint32_t j = 0; j < c->m; ++j) {
+                ckpt_ctx *o = c->members[j];
+                if ((rc = set_dev(o)) || (rc = stage_finish(o))) goto bad;
+                o->issued = true;
+                o->requested = false;
+                o->st.snapshots++;
+            }
+            set_dev(c);
+        }
+        if (id) *id = my_id;
+        return CKPT_OK;
+    bad:
+        for (uint32_t j = 0; j < c->m; ++j) make_sticky(c->members[j], rc);
+        return rc;
+    }
+    if ((rc = begin_member(c, caller, B))) return rc;
+    for (uint64_t k = 0; k < c->op_NB; ++k) {
+        if ((rc = stage_pack(c, k)) || (rc = stage_xor(c, k)) || (rc = stage_copy(c, k))) {
+            make_sticky(c, rc);
+            return rc;
+        }
+    }
+    if ((rc = stage_finish(c))) {
+        make_sticky(c, rc);
+        return rc;
+    }
+    c->pending_id = my_id;
+    c->issued = true;
+    c->st.snapshots++;
+    if (id) *id = my_id;
+    return CKPT_OK;
+}
+
+extern "C" int ckpt_fence(ckpt_ctx *c, uint64_t id, void *stream) {
+    if (!c) return fail(CKPT_EINVAL, "fence: null");
+    if (id == 0 || id >= c->next_id) return fail(CKPT_EINVAL, "fence: unknown snapshot id");
+    if (id != c->pending_id) return CKPT_OK;  // already waited: nothing reads the tensors
+    if (!c->issued) return fail(CKPT_ESTATE, "fence: LOCAL group snapshot not issued yet (members missing)");
+    int rc = set_dev(c);
+    if (rc) return rc;
+    CUDA_TRY(cudaStreamWaitEvent((cudaStream_t)stream, c->ev_pack_all, 0));
+    return CKPT_OK;
+}
+
+// Host-side wait on a stream with a timeout (peers that died never signal).
+static int sync_stream_timeout(ckpt_ctx *c, cudaStream_t s, const char *what) {
+    double limit = 600.0;
+    if (const char *e = getenv("CKPT_TIMEOUT_S")) limit = atof(e);
+    auto t0 = std::chrono::steady_clock::now();
+    for (;;) {
+        cudaError_t e = cudaStreamQuery(s);
+        if (e == cudaSuccess) return CKPT_OK;
+        if (e != cudaErrorNotReady) return fail(CKPT_ECUDA, "%s: %s", what, cudaGetErrorString(e));
+        double el = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+        if (el > limit) {
+            // release our own stream waits so the context can be destroyed
+            cudaMemset(c->flags, 0x7f, kFlagBytes);
+            return fail(CKPT_EPEER, "%s: timed out after %.0f s waiting for peers", what, limit);
+        }
+        std::this_thread::sleep_for(std::chrono::microseconds(el < 0.01 ? 20 : 200));
+    }
+}
+
+static int wait_done_all(ckpt_ctx *c, uint32_t done_seq) {
+    int rc;
+    cudaStream_t ss[3] = {c->sP, c->sX, c->sC};
+    for (auto s : ss)
+        if ((rc = sync_stream_timeout(c, s, "wait"))) return rc;
+    if (c->m >= 2) {
+        if (c->transport == CKPT_GROUP_IPC) {
+            if ((rc = wait_all(c, c->sW, kDone, done_seq, 0))) return rc;
+            if ((rc = sync_stream_timeout(c, c->sW, "wait(peers)"))) return rc;
+        } else {
+            for (uint32_t j = 0; j < c->m; ++j) {
+                ckpt_ctx *o = c->members[j];
+                if (o == c) continue;
+                CUDA_TRY(cudaEventSynchronize(o->ev_done));
+            }
+        }
+    }
+    return CKPT_OK;
+}
+
+extern "C" int ckpt_wait(ckpt_ctx *c, uint64_t id) {
+    if (!c) return fail(CKPT_EINVAL, "wait: null");
+    if (id == 0 || id >= c->next_id) return fail(CKPT_ESTATE, "wait: unknown snapshot id %llu", (unsigned long long)id);
+    if (id != c->pending_id) return c->completed_id >= id ? CKPT_OK : fail(CKPT_ESTATE, "wait: snapshot %llu was not committed", (unsigned long long)id);
+    if (!c->issued) return fail(CKPT_ESTATE, "wait: LOCAL group snapshot not issued yet (members missing)");
+    int rc = set_dev(c);
+    if (rc) return rc;
+    rc = wait_done_all(c, c->op_seq_base + (uint32_t)c->op_NB + 1);
+    if (!rc) rc = check_sticky(c);
+    if (!rc && (c->opt.flags & CKPT_OPT_TIMING)) {
+        rc = harvest_timing(c);
+        float ms = 0;
+        if (!rc && cudaEventElapsedTime(&ms, c->ev_t0, c->ev_t1) == cudaSuccess) c->st.last_snapshot_ms = ms;
+        cudaGetLastError();
+    }
+    c->pending_id = 0;
+    c->issued = false;
+    if (rc) {  // never commit a failed snapshot (S.431)
+        make_sticky(c, rc);
+        return rc;
+    }
+    c->completed = c->ongoing;
+    c->completed_id = id;
+    if (c->nbuf == 2) c->ongoing ^= 1;
+    return CKPT_OK;
+}
+
+// ------------------------------------------------------------------ load ------------
+extern "C" int ckpt_load(ckpt_ctx *c, void *stream) {
+    if (!c) return fail(CKPT_EINVAL, "load: null");
+    if (!c->registered) return fail(CKPT_ESTATE, "load: not registered");
+    int rc = check_sticky(c);
+    if (rc) return rc;
+    if (c->pending_id || c->requested) return fail(CKPT_ESTATE, "load: a snapshot is in flight");
+    if (c->rebuild_requested) return fail(CKPT_ESTATE, "load: a LOCAL group rebuild is not complete");
+    if (!c->grouped || c->completed < 0) return fail(CKPT_ENOSNAP, "load: no completed snapshot");
+    if ((rc = set_dev(c))) return rc;
+    cudaStream_t caller = (cudaStream_t)stream;
+    // op geometry: bucket = ring slot (or the default bucket in full-copy mode)
+    const uint32_t saved_seq = c->seq;
+    if ((rc = prepare_op(c, effective_bucket(c, 0)))) return rc;
+    c->seq = saved_seq;  // local op: no group sequence numbers consumed
+    CUDA_TRY(cudaEventRecord(c->ev_capture, caller));
+    CUDA_TRY(cudaStreamWaitEvent(c->sC, c->ev_capture, 0));
+    const uint8_t *img = c->hdata[c->completed].p;
+    for (uint64_t k = 0; k < c->op_NB; ++k) {
+        const uint32_t s = slot_of(c, k);
+        const uint64_t bb = bucket_begin(c, k);
+        const uint64_t v = valid_in_bucket(c->L, bb, bucket_end(c, k));
+        if (!v) continue;
+        if (ring_reuse(c, k)) CUDA_TRY(cudaStreamWaitEvent(c->sC, c->ev_kdone[s], 0));
+        CUDA_TRY(cudaMemcpyAsync(slot_ptr(c, c->staging, k), img + bb, v, cudaMemcpyHostToDevice, c->sC));
+        c->st.h2d_bytes += v;
+        CUDA_TRY(cudaEventRecord(c->ev_h2d[s], c->sC));
+        CUDA_TRY(cudaStreamWaitEvent(c->sP, c->ev_h2d[s], 0));
+        if ((rc = do_pack(c, k, slot_ptr(c, c->staging, k), c->sP, true))) return rc;
+        CUDA_TRY(cudaEventRecord(c->ev_kdone[s], c->sP));
+    }
+    CUDA_TRY(cudaStreamWaitEvent(c->sP, c->ev_capture, 0));
+    CUDA_TRY(cudaEventRecord(c->ev_pack_all, c->sP));
+    CUDA_TRY(cudaStreamWaitEvent(caller, c->ev_pack_all, 0));
+    c->st.loads++;
+    if (c->opt.flags & CKPT_OPT_TIMING) {
+        CUDA_TRY(cudaStreamSynchronize(c->sP));
+        rc = harvest_timing(c);
+    }
+    return rc;
+}
+
+// ------------------------------------------------------------------ rebuild ---------
+// Per bucket b (slot s), lost member kl:
+//   survivor j: C: [reuse: own kernel(b-n) done, REL(b-n) from all] H2D data+parity -> READY(b)
+//               X: own H2D, READY(b) from all -> rebuild row j into kl's slot -> REL(b)
+//   lost kl   : X: [reuse: own D2H(b-n)] READY(b) ; READY(b) from all -> encode row kl -> REL(b)
+//               C: REL(b) from all, own encode -> D2H data + parity into its image
+static int rb_stage1(ckpt_ctx *c, uint64_t b, uint32_t kl) {
+    const uint32_t s = slot_of(c, b);
+    const uint64_t bb = bucket_begin(c, b), be = bucket_end(c, b);
+    int rc;
+    if (c->me != kl) {
+        if (ring_reuse(c, b)) {
+            CUDA_TRY(cudaStreamWaitEvent(c->sC, c->ev_kdone[s], 0));
+            if ((rc = wait_all(c, c->sC, kRel, bucket_seq(c, b - c->n_slots), s))) return rc;
+        }
+        const uint64_t v = valid_in_bucket(c->L, bb, be);
+        if (v) CUDA_TRY(cudaMemcpyAsync(slot_ptr(c, c->staging, b), c->hdata[c->completed].p + bb, v, cudaMemcpyHostToDevice, c->sC));
+        const uint64_t pb = (be - bb) / (c->m - 1);
+        CUDA_TRY(cudaMemcpyAsync(parity_slot_ptr(c, b), c->hpar[c->completed].p + bb / (c->m - 1), pb, cudaMemcpyHostToDevice, c->sC));
+        c->st.h2d_bytes += v + pb;
+        CUDA_TRY(cudaEventRecord(c->ev_h2d[s], c->sC));
+        return sig_signal(c, c->sC, kReady, bucket_seq(c, b), s);
+    }
+    if (ring_reuse(c, b)) {
+        CUDA_TRY(cudaStreamWaitEvent(c->sX, c->ev_d2h_data[s], 0));
+        CUDA_TRY(cudaStreamWaitEvent(c->sX, c->ev_d2h_par[s], 0));
+    }
+    return sig_signal(c, c->sX, kReady, bucket_seq(c, b), s);
+}
+
+static int rb_stage2(ckpt_ctx *c, uint64_t b, uint32_t kl) {
+    const uint32_t s = slot_of(c, b);
+    int rc;
+    if (c->me != kl) CUDA_TRY(cudaStreamWaitEvent(c->sX, c->ev_h2d[s], 0));
+    if ((rc = wait_all(c, c->sX, kReady, bucket_seq(c, b), s))) return rc;
+    if (c->me != kl)
+        rc = do_rebuild_row(c, b, kl, c->sX);
+    else
+        rc = do_encode(c, b, c->sX);
+    if (rc) return rc;
+    CUDA_TRY(cudaEventRecord(c->ev_kdone[s], c->sX));
+    return sig_signal(c, c->sX, kRel, bucket_seq(c, b), s);
+}
+
+static int rb_stage3(ckpt_ctx *c, uint64_t b, uint32_t kl) {
+    if (c->me != kl) return CKPT_OK;
+    const uint32_t s = slot_of(c, b);
+    const uint64_t bb = bucket_begin(c, b), be = bucket_end(c, b);
+    int rc;
+    if ((rc = wait_all(c, c->sC, kRel, bucket_seq(c, b), s))) return rc;
+    CUDA_TRY(cudaStreamWaitEvent(c->sC, c->ev_kdone[s], 0));
+    const uint64_t v = valid_in_bucket(c->L, bb, be);
+    if (v) CUDA_TRY(cudaMemcpyAsync(c->hdata[c->ongoing].p + bb, slot_ptr(c, c->staging, b), v, cudaMemcpyDeviceToHost, c->sC));
+    CUDA_TRY(cudaEventRecord(c->ev_d2h_data[s], c->sC));
+    const uint64_t pb = (be - bb) / (c->m - 1);
+    CUDA_TRY(cudaMemcpyAsync(c->hpar[c->ongoing].p + bb / (c->m - 1), parity_slot_ptr(c, b), pb, cudaMemcpyDeviceToHost, c->sC));
+    CUDA_TRY(cudaEventRecord(c->ev_d2h_par[s], c->sC));
+    c->st.d2h_bytes += v + pb;
+    return CKPT_OK;
+}
+
+static int rb_finish(ckpt_ctx *c) {
+    // DONE after every local stream finished (the lost member's D2H is the last step)
+    CUDA_TRY(cudaEventRecord(c->ev_pack_all, c->sX));
+    CUDA_TRY(cudaStreamWaitEvent(c->sC, c->ev_pack_all, 0));
+    CUDA_TRY(cudaEventRecord(c->ev_done, c->sC));
+    return sig_signal(c, c->sC, kDone, c->op_seq_base + (uint32_t)c->op_NB + 1, 0);
+}
+
+static int rb_commit(ckpt_ctx *c, uint32_t kl, uint64_t version) {
+    int rc = wait_done_all(c, c->op_seq_base + (uint32_t)c->op_NB + 1);
+    if (!rc && (c->opt.flags & CKPT_OPT_TIMING)) rc = harvest_timing(c);
+    if (rc) {
+        make_sticky(c, rc);
+        return rc;
+    }
+    if (c->me == kl) {
+        // the image's zero pad [L, L*) is structural (Q5); a lost host image had it
+        // overwritten, and the D2H above only covers [0, L)
+        if (c->Lstar > c->L) memset(c->hdata[c->ongoing].p + c->L, 0, c->Lstar - c->L);
+        c->completed = c->ongoing;
+        c->completed_id = version;
+        if (c->nbuf == 2) c->ongoing ^= 1;
+    }
+    c->st.rebuilds++;
+    return CKPT_OK;
+}
+
+extern "C" int ckpt_rebuild(ckpt_ctx *c, int32_t lost, void *stream) {
+    if (!c) return fail(CKPT_EINVAL, "rebuild: null");
+    if (!c->registered || !c->grouped) return fail(CKPT_ESTATE, "rebuild: not protected");
+    if (c->m < 2) return fail(CKPT_EUNRECOVERABLE, "rebuild: a group of one has no redundancy (P.460)");
+    if (lost < 0 || (uint32_t)lost >= c->m) return fail(CKPT_EINVAL, "rebuild: lost rank %d out of range", lost);
+    int rc = check_sticky(c);
+    if (rc) return rc;
+    if (c->pending_id || c->requested) return fail(CKPT_ESTATE, "rebuild: a snapshot is in flight");
+    const uint32_t kl = (uint32_t)lost;
+    if (c->me != kl && c->completed < 0)
+        return fail(CKPT_EUNRECOVERABLE, "rebuild: survivor %u has no completed image (more than one loss)", c->me);
+    if ((rc = set_dev(c))) return rc;
+    cudaStream_t caller = (cudaStream_t)stream;
+    const uint64_t B = effective_bucket(c, 0);
+    if (c->transport == CKPT_GROUP_LOCAL) {
+        c->rebuild_requested = true;
+        c->rebuild_lost = lost;
+        CUDA_TRY(cudaEventRecord(c->ev_capture, caller));
+        for (uint32_t j = 0; j < c->m; ++j)
+            if (!c->members[j]->rebuild_requested) return CKPT_OK;  // issued by the last member
+        uint64_t version = 0;
+        for (uint32_t j = 0; j < c->m; ++j) {
+            ckpt_ctx *o = c->members[j];
+            if (o->rebuild_lost != lost) return fail(CKPT_EINVAL, "rebuild: members disagree on the lost rank");
+            if (j != kl) {
+                if (o->completed < 0) return fail(CKPT_EUNRECOVERABLE, "rebuild: survivor %u has no completed image", j);
+                version = std::max(version, o->completed_id);
+            }
+        }
+        for (uint32_t j = 0; j < c->m; ++j) {
+            ckpt_ctx *o = c->members[j];
+            if ((rc = set_dev(o)) || (rc = prepare_op(o, B))) goto bad;
+            CUDA_TRY(cudaStreamWaitEvent(o->sC, o->ev_capture, 0));
+            CUDA_TRY(cudaStreamWaitEvent(o->sX, o->ev_capture, 0));
+        }
+        for (uint64_t b = 0; b < c->op_NB; ++b) {
+            for (uint32_t j = 0; j < c->m; ++j)
+                if ((rc = set_dev(c->members[j])) || (rc = rb_stage1(c->members[j], b, kl))) goto bad;
+            for (uint32_t j = 0; j < c->m; ++j)
+                if ((rc = set_dev(c->members[j])) || (rc = rb_stage2(c->members[j], b, kl))) goto bad;
+            for (uint32_t j = 0; j < c->m; ++j)
+                if ((rc = set_dev(c->members[j])) || (rc = rb_stage3(c->members[j], b, kl))) goto bad;
+        }
+        for (uint32_t j = 0; j < c->m; ++j)
+            if ((rc = set_dev(c->members[j])) || (rc = rb_finish(c->members[j]))) goto bad;
+        for (uint32_t j = 0; j < c->m; ++j) {
+            ckpt_ctx *o = c->members[j];
+            if ((rc = set_dev(o)) || (rc = rb_commit(o, kl, version))) goto bad;
+            o->rebuild_requested = false;
+        }
+        return set_dev(c);
+    bad:
+        for (uint32_t j = 0; j < c->m; ++j) {
+            make_sticky(c->members[j], rc);
+            c->members[j]->rebuild_requested = false;
+        }
+        return rc;
+    }
+    // IPC: every member runs its own side; the version is the survivors' completed id
+    if ((rc = prepare_op(c, B))) return rc;
+    CUDA_TRY(cudaEventRecord(c->ev_capture, caller));
+    CUDA_TRY(cudaStreamWaitEvent(c->sC, c->ev_capture, 0));
+    CUDA_TRY(cudaStreamWaitEvent(c->sX, c->ev_capture, 0));
+    for (uint64_t b = 0; b < c->op_NB; ++b) {
+        if ((rc = rb_stage1(c, b, kl)) || (rc = rb_stage2(c, b, kl)) || (rc = rb_stage3(c, b, kl))) {
+            make_sticky(c, rc);
+            return rc;
+        }
+    }
+    if ((rc = rb_finish(c))) {
+        make_sticky(c, rc);
+        return rc;
+    }
+    return rb_commit(c, kl, c->me == kl ? c->next_id - 1 : c->completed_id);
+}
+
+// ------------------------------------------------------------------ misc ------------
+extern "C" int ckpt_forget(ckpt_ctx *c, uint8_t poison) {
+    if (!c) return fail(CKPT_EINVAL, "forget: null");
+    if (c->pending_id || c->requested) return fail(CKPT_ESTATE, "forget: a snapshot is in flight");
+    for (int i = 0; i < 2; ++i) {
+        if (c->hdata[i].p) memset(c->hdata[i].p, poison, c->Lstar);
+        if (c->hpar[i].p && c->m >= 2) memset(c->hpar[i].p, poison, c->Lstar / (c->m - 1));
+    }
+    c->completed = -1;
+    c->completed_id = 0;
+    return CKPT_OK;
+}
+
+extern "C" int ckpt_host_view(const ckpt_ctx *c, int which, const void **data, uint64_t *dlen, const void **par,
+                              uint64_t *plen) {
+    if (!c || (which != 0 && which != 1)) return fail(CKPT_EINVAL, "host_view: bad args");
+    if (!c->grouped) return fail(CKPT_ENOSNAP, "host_view: no host arena yet");
+    int idx = which == 0 ? c->completed : c->ongoing;
+    if (idx < 0) return fail(CKPT_ENOSNAP, "host_view: no completed snapshot");
+    if (data) *data = c->hdata[idx].p;
+    if (dlen) *dlen = c->Lstar;
+    if (par) *par = c->m >= 2 ? c->hpar[idx].p : nullptr;
+    if (plen) *plen = c->m >= 2 ? c->Lstar / (c->m - 1) : 0;
+    return CKPT_OK;
+}
+
+extern "C" int ckpt_get_stats(const ckpt_ctx *c, ckpt_stats *out) {
+    if (!c || !out) return fail(CKPT_EINVAL, "get_stats: null");
+    *out = c->st;
+    return CKPT_OK;
+}
+
+extern "C" int ckpt_stats_reset(ckpt_ctx *c) {
+    if (!c) return fail(CKPT_EINVAL, "stats_reset: null");
+    c->st = ckpt_stats{};
+    return CKPT_OK;
+}

@@ -1,0 +1,91 @@
+"""CPU-only checks of the C ABI library: it builds, loads, exports every symbol
+include/*.h declares, its host-only planner agrees with the oracle's layout pins, and
+it refuses to run without a GPU (no CPU fallback)."""
+import os
+import re
+
+import numpy as np
+import pytest
+
+import oracle
+from conftest import ROOT, golden
+
+
+@pytest.fixture(scope="module")
+def C():
+    from paper_2310_12670_b200 import build, ckpt
+    build.build()
+    return ckpt
+
+
+def declared(header):
+    src = open(os.path.join(ROOT, "include", header)).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b((?:ckpt|reft)_[a-z0-9_]+)\s*\(", src)))
+
+
+def test_every_declared_symbol_is_exported(C):
+    import ctypes
+    lib = ctypes.CDLL(C.LIB_PATH)
+    names = declared("ckpt.h")
+    assert len(names) >= 20
+    for n in names:
+        assert hasattr(lib, n), f"libreft_ckpt.so does not export {n}"
+    synth = ctypes.CDLL(C.SYNTH_PATH)
+    for n in declared("reft_synth.h"):
+        assert hasattr(synth, n), n
+
+
+def test_library_is_sm100a():
+    import subprocess
+    from paper_2310_12670_b200 import build
+    libs = build.build()
+    out = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "--list-elf", libs["libreft_ckpt.so"]],
+                         capture_output=True, text=True).stdout
+    assert "sm_100a" in out
+    sass = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "-sass", libs["libreft_ckpt.so"]],
+                          capture_output=True, text=True).stdout
+    assert "UBLKCP" in sass          # TMA 1-D bulk copies in the TMA pack kernel
+    assert "LDG.E.128" in sass       # 128-bit loads in the LSU pack / XOR kernels
+
+
+def test_plan_layout_matches_oracle_golden(C):
+    g = golden("layout_a256.txt")
+    sizes = [int(x) for x in g["sizes"][0]]
+    assert C.ckpt_plan_layout(sizes, 256) == oracle.layout(sizes, 256)
+    assert C.ckpt_plan_layout(sizes, 256)[0] == [int(x) for x in g["offsets"][0]]
+    for m, u, Ls, ue in g["common"]:
+        assert C.ckpt_plan_common([1280, 768, 1024][: int(m)], int(u)) == (int(Ls), int(ue))
+
+
+def test_plan_random_vs_oracle(C):
+    rng = np.random.default_rng(5)
+    for _ in range(200):
+        sizes = rng.integers(1, 1 << 20, size=int(rng.integers(1, 30))).tolist()
+        align = int(2 ** rng.integers(4, 13))
+        assert C.ckpt_plan_layout(sizes, align) == oracle.layout(sizes, align)
+        m = int(rng.integers(1, 9))
+        Ls = rng.integers(1, 1 << 24, size=m).tolist()
+        u = int(rng.choice([0, 16, 4096, 65536]))
+        assert C.ckpt_plan_common(Ls, u) == oracle.common_length(Ls, u)
+
+
+def test_no_gpu_means_error_not_fallback(C):
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    with pytest.raises(C.CkptError) as e:
+        C.ckpt_create(0)
+    assert e.value.code == C.CKPT_ECUDA
+    assert "no CPU fallback" in str(e.value)
+
+
+def test_strerror_and_version(C):
+    assert C.ckpt_strerror(C.CKPT_EUNRECOVERABLE).startswith("unrecoverable")
+    assert C.ckpt_strerror(12345) == "unknown error"
+    assert "sm_100a" in C.ckpt_version()
+
+
+def test_options_defaults(C):
+    o = C.ckpt_options_default()
+    assert (o.align, o.stripe_unit, o.bucket_bytes, o.n_slots, o.host_buffers) == (256, 65536, 64 << 20, 4, 2)

@@ -1,0 +1,300 @@
+"""GPU parity: the CUDA path through the C ABI vs the CPU oracle, bit-exact.
+
+Single-GPU cases use CKPT_GROUP_LOCAL groups (m contexts on cuda:0, the same kernels
+and the same per-member stream schedule as the one-process-per-GPU IPC transport,
+ordered with CUDA events instead of cross-process flags)."""
+import numpy as np
+import pytest
+
+import oracle
+import synth
+from gpu_util import assert_bytes_equal, need_gpu, oracle_image, oracle_tensor_bytes, tensor_bytes
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def torch():
+    return need_gpu()
+
+
+@pytest.fixture(scope="module")
+def C(torch):
+    from paper_2310_12670_b200 import ckpt
+    return ckpt
+
+
+def make_ctx(C, specs_ts, **opt):
+    from synth.gpu import descriptors
+    specs, ts = specs_ts
+    o = C.ckpt_options_default(**opt)
+    ctx = C.ckpt_create(0, o)
+    C.ckpt_register(ctx, descriptors(ts, specs))
+    return ctx
+
+
+def tiny(rank, n=9, misalign=0, device="cuda:0"):
+    from synth.gpu import alloc_state, fill_state
+    specs = synth.config_tensors(f"tiny_{n}", rank)
+    ts = alloc_state(specs, device, misalign)
+    fill_state(ts, rank)
+    return specs, ts
+
+
+# ------------------------------------------------------------------ m = 1 ---------
+@pytest.mark.parametrize("n_slots,bucket,flags", [
+    (0, 0, 0), (2, 4096, 0), (4, 65536, 0), (3, 1 << 20, 0),
+    (0, 0, 0x2), (2, 65536, 0x2), (4, 4096, 0x2)])
+@pytest.mark.parametrize("misalign", [0, 1])
+def test_snapshot_unprotected_matches_oracle(torch, C, n_slots, bucket, flags, misalign):
+    st = tiny(0, n=11, misalign=misalign)
+    specs, ts = st
+    ctx = make_ctx(C, st, n_slots=n_slots, bucket_bytes=max(bucket, 4096), flags=flags)
+    try:
+        assert C.ckpt_protect(ctx, 1, 0) == C.CKPT_EUNAVAIL
+        sid = C.ckpt_snapshot(ctx, bucket)
+        C.ckpt_wait(ctx, sid)
+        g = C.ckpt_geometry(ctx)
+        want, off, L = oracle_image(specs, 0, g["L_star"])
+        assert g["L"] == L == g["L_star"]
+        data, par = C.ckpt_host_view(ctx, 0, copy=True)
+        assert par is None
+        assert_bytes_equal(data, want, "data image")
+        assert [C.ckpt_tensor_offset(ctx, t) for t in range(len(specs))] == off
+        # load: mutate the live tensors (a later step), restore, compare
+        from synth.gpu import fill_state
+        fill_state(ts, 0, seed=999, xor_mode=1)
+        C.ckpt_load(ctx)
+        torch.cuda.synchronize()
+        for t, (x, w) in enumerate(zip(ts, oracle_tensor_bytes(specs, 0))):
+            assert_bytes_equal(tensor_bytes(x), w, f"tensor {t} after load")
+    finally:
+        C.ckpt_destroy(ctx)
+
+
+def test_register_errors(torch, C):
+    ctx = C.ckpt_create(0)
+    try:
+        with pytest.raises(C.CkptError) as e:
+            C.ckpt_register(ctx, [])
+        assert e.value.code == C.CKPT_EINVAL
+        x = torch.empty(0, device="cuda:0")
+        with pytest.raises(C.CkptError):
+            C.ckpt_register(ctx, [(x.data_ptr() or 16, 0, 0, 0, 0, "z")])
+        h = torch.empty(16)  # host memory is rejected
+        with pytest.raises(C.CkptError) as e:
+            C.ckpt_register(ctx, [h])
+        assert e.value.code == C.CKPT_EINVAL
+        with pytest.raises(C.CkptError) as e:
+            C.ckpt_load(ctx)
+        assert e.value.code in (C.CKPT_ESTATE, C.CKPT_ENOSNAP)
+    finally:
+        C.ckpt_destroy(ctx)
+
+
+def test_single_byte_tensor_and_busy(torch, C):
+    x = torch.arange(1, dtype=torch.uint8, device="cuda:0") + 7
+    ctx = C.ckpt_create(0, C.ckpt_options_default(n_slots=2, bucket_bytes=4096))
+    try:
+        C.ckpt_register(ctx, [x])
+        sid = C.ckpt_snapshot(ctx)
+        with pytest.raises(C.CkptError) as e:
+            C.ckpt_snapshot(ctx)
+        assert e.value.code == C.CKPT_EBUSY
+        C.ckpt_wait(ctx, sid)
+        d, _ = C.ckpt_host_view(ctx, 0, copy=True)
+        assert d.size == 256 and d[0] == 7 and not d[1:].any()
+    finally:
+        C.ckpt_destroy(ctx)
+
+
+# ------------------------------------------------------------------ LOCAL groups --
+def make_group(torch, C, m, unit, n_slots=0, bucket=1 << 20, flags=0, misalign=0):
+    states = [tiny(j, n=5 + j % 3, misalign=misalign) for j in range(m)]
+    ctxs = [make_ctx(C, st, n_slots=n_slots, bucket_bytes=bucket, stripe_unit=unit, flags=flags)
+            for st in states]
+    C.protect_local(ctxs)
+    return states, ctxs
+
+
+def snapshot_group(C, ctxs, bucket=0):
+    ids = [C.ckpt_snapshot(c, bucket) for c in ctxs]
+    for c, i in zip(ctxs, ids):
+        C.ckpt_wait(c, i)
+
+
+def expected_group(states, Lstar, unit):
+    Ds = [oracle_image(specs, j, Lstar)[0] for j, (specs, _) in enumerate(states)]
+    Ps = oracle.encode_all(Ds, unit) if len(Ds) > 1 else [None]
+    return Ds, Ps
+
+
+@pytest.mark.parametrize("m", [2, 3, 4, 8])
+@pytest.mark.parametrize("unit,n_slots,bucket", [(65536, 0, 1 << 20), (4096, 3, 1 << 20), (16, 2, 4096),
+                                                 (0, 0, 1 << 20), (65536, 4, 1 << 20)])
+def test_group_encode_matches_oracle(torch, C, m, unit, n_slots, bucket):
+    if unit == 65536 and n_slots and (m - 1) * unit > bucket:
+        pytest.skip("stripe larger than ring slot")
+    states, ctxs = make_group(torch, C, m, unit, n_slots, bucket)
+    try:
+        snapshot_group(C, ctxs)
+        g = C.ckpt_geometry(ctxs[0])
+        Ls, ue = oracle.common_length([oracle.layout([s.nbytes for s in sp])[1] for sp, _ in states], unit)
+        assert (g["L_star"], g["unit"], g["m"]) == (Ls, ue, m)
+        Ds, Ps = expected_group(states, Ls, ue)
+        for j, c in enumerate(ctxs):
+            d, p = C.ckpt_host_view(c, 0, copy=True)
+            assert_bytes_equal(d, Ds[j], f"rank {j} data")
+            assert_bytes_equal(p, Ps[j], f"rank {j} parity")
+    finally:
+        for c in ctxs:
+            C.ckpt_destroy(c)
+
+
+@pytest.mark.parametrize("m,unit,n_slots,flags", [(2, 4096, 0, 0), (3, 4096, 2, 0), (4, 65536, 0, 0x2),
+                                                  (8, 1024, 3, 0), (8, 0, 0, 0), (5, 64, 2, 0x2)])
+def test_group_drill_rebuild_every_rank(torch, C, m, unit, n_slots, flags):
+    """Failure drill (Q12): rank k loses tensors and host image; rebuild + load."""
+    from synth.gpu import fill_state
+    states, ctxs = make_group(torch, C, m, unit, n_slots, bucket=max(1 << 16, (m - 1) * unit * 2), flags=flags,
+                              misalign=1)
+    try:
+        snapshot_group(C, ctxs)
+        g = C.ckpt_geometry(ctxs[0])
+        Ds, Ps = expected_group(states, g["L_star"], g["unit"])
+        for k in range(m):
+            # later training steps mutate every rank; rank k is lost entirely
+            for j, (specs, ts) in enumerate(states):
+                fill_state(ts, j, seed=4242 + k, xor_mode=1)
+            C.ckpt_forget(ctxs[k], 0xA5)
+            for t in states[k][1]:
+                t.view(torch.uint8).fill_(0xA5)
+            with pytest.raises(C.CkptError) as e:
+                C.ckpt_load(ctxs[k])
+            assert e.value.code == C.CKPT_ENOSNAP
+            for c in ctxs:
+                C.ckpt_rebuild(c, k)
+            d, p = C.ckpt_host_view(ctxs[k], 0, copy=True)
+            assert_bytes_equal(d, Ds[k], f"rebuilt data of rank {k}")
+            assert_bytes_equal(p, Ps[k], f"re-encoded parity of rank {k}")
+            for c in ctxs:
+                C.ckpt_load(c)
+            torch.cuda.synchronize()
+            for j, (specs, ts) in enumerate(states):
+                for t, (x, w) in enumerate(zip(ts, oracle_tensor_bytes(specs, j))):
+                    assert_bytes_equal(tensor_bytes(x), w, f"k={k}: rank {j} tensor {t} after load")
+    finally:
+        for c in ctxs:
+            C.ckpt_destroy(c)
+
+
+def test_two_losses_unrecoverable(torch, C):
+    states, ctxs = make_group(torch, C, 4, 4096)
+    try:
+        snapshot_group(C, ctxs)
+        C.ckpt_forget(ctxs[1])
+        with pytest.raises(C.CkptError) as e:  # survivor 1 lost its image too
+            C.ckpt_rebuild(ctxs[1], 0)
+        assert e.value.code == C.CKPT_EUNRECOVERABLE
+    finally:
+        for c in ctxs:
+            C.ckpt_destroy(c)
+
+
+def test_bucket_size_invariance_and_commit(torch, C):
+    """I8: images do not depend on the bucket size; commit keeps the previous image
+    readable until the next snapshot is waited (P.553-554, S.431)."""
+    from synth.gpu import fill_state
+    states, ctxs = make_group(torch, C, 4, 4096, n_slots=0)
+    try:
+        snapshot_group(C, ctxs, bucket=3 * 4096)
+        first = [tuple(x.copy() for x in C.ckpt_host_view(c, 0, copy=True)) for c in ctxs]
+        snapshot_group(C, ctxs, bucket=3 * 4096 * 7)
+        for c, (d0, p0) in zip(ctxs, first):
+            d, p = C.ckpt_host_view(c, 0, copy=True)
+            assert_bytes_equal(d, d0, "data vs bucket size")
+            assert_bytes_equal(p, p0, "parity vs bucket size")
+        # mutate, snapshot, do NOT wait yet: completed still holds the old image
+        for j, (_, ts) in enumerate(states):
+            fill_state(ts, j, seed=7, xor_mode=1)
+        ids = [C.ckpt_snapshot(c) for c in ctxs]
+        for c, (d0, _) in zip(ctxs, first):
+            assert_bytes_equal(C.ckpt_host_view(c, 0, copy=True)[0], d0, "completed image during snapshot")
+        for c, i in zip(ctxs, ids):
+            C.ckpt_wait(c, i)
+        assert not np.array_equal(C.ckpt_host_view(ctxs[0], 0, copy=True)[0], first[0][0])
+    finally:
+        for c in ctxs:
+            C.ckpt_destroy(c)
+
+
+# ------------------------------------------------------------------ full sizes ----
+def test_c1_16mib_m8_full_parity(torch, C):
+    """BASELINE config 1: 8 ranks x 16 MiB fp32, encode + rebuild of every rank,
+    compared element by element with the oracle (launch configuration of bench)."""
+    from synth.gpu import make_rank_state, descriptors
+    m = 8
+    states = [make_rank_state("c1_16mb_fp32_m8", j, "cuda:0") for j in range(m)]
+    ctxs = []
+    for specs, ts in states:
+        c = C.ckpt_create(0, C.ckpt_options_default(n_slots=0))
+        C.ckpt_register(c, descriptors(ts, specs))
+        ctxs.append(c)
+    try:
+        C.protect_local(ctxs)
+        snapshot_group(C, ctxs)
+        g = C.ckpt_geometry(ctxs[0])
+        assert g["L_star"] == 16973824 and g["unit"] == 65536
+        Ds, Ps = expected_group(states, g["L_star"], g["unit"])
+        for j, c in enumerate(ctxs):
+            d, p = C.ckpt_host_view(c, 0, copy=True)
+            assert p.size == 2424832
+            assert_bytes_equal(d, Ds[j], f"rank {j} data")
+            assert_bytes_equal(p, Ps[j], f"rank {j} parity")
+        for k in (0, 5, 7):
+            C.ckpt_forget(ctxs[k])
+            for c in ctxs:
+                C.ckpt_rebuild(c, k)
+            d, p = C.ckpt_host_view(ctxs[k], 0, copy=True)
+            assert_bytes_equal(d, Ds[k], f"rebuilt rank {k}")
+            assert_bytes_equal(p, Ps[k], f"re-encoded parity rank {k}")
+    finally:
+        for c in ctxs:
+            C.ckpt_destroy(c)
+
+
+def test_c2_7b_tp8_rank_sampled(torch, C):
+    """BASELINE config 2 at full size on one GPU (m = 1, the N=1 bench launch
+    configuration): 1164 tensors, 11.8 GB.  Sampled check: head and tail of every
+    tensor's bytes in the host image vs the oracle's generator; load round trip on a
+    sample of tensors."""
+    from synth.gpu import make_rank_state, descriptors, fill_state
+    specs, ts = make_rank_state("c2_7b_tp8", 3, "cuda:0")
+    assert len(specs) == 1164 and sum(s.nbytes for s in specs) == 11795488768
+    ctx = C.ckpt_create(0, C.ckpt_options_default(n_slots=4, bucket_bytes=64 << 20))
+    try:
+        C.ckpt_register(ctx, descriptors(ts, specs))
+        sid = C.ckpt_snapshot(ctx)
+        C.ckpt_wait(ctx, sid)
+        data, _ = C.ckpt_host_view(ctx, 0)  # zero-copy view: slices are copied below
+        rng = np.random.default_rng(0)
+        for t, s in enumerate(specs):
+            off = C.ckpt_tensor_offset(ctx, t)
+            n = min(s.nbytes, 4096)
+            assert_bytes_equal(data[off:off + n].copy(), oracle.fill(synth.SEED, 3, t, n), f"tensor {t} head")
+            tail0 = s.nbytes - n
+            assert_bytes_equal(data[off + tail0:off + s.nbytes].copy(), oracle.fill(synth.SEED, 3, t, n, tail0),
+                               f"tensor {t} tail")
+            pad_end = C.ckpt_tensor_offset(ctx, t + 1) if t + 1 < len(specs) else data.size
+            assert not data[off + s.nbytes:pad_end].any()
+        del data
+        sample = rng.choice(len(specs), 6, replace=False)
+        fill_state(ts, 3, seed=1, xor_mode=1)
+        C.ckpt_load(ctx)
+        torch.cuda.synchronize()
+        for t in sample:
+            n = min(specs[t].nbytes, 1 << 20)
+            got = tensor_bytes(ts[t].view(torch.uint8)[:n])
+            assert_bytes_equal(got, oracle.fill(synth.SEED, 3, int(t), n), f"tensor {t} after load")
+    finally:
+        C.ckpt_destroy(ctx)
