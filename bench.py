@@ -39,12 +39,20 @@ def parse():
     p.add_argument("--bucket", type=int, default=64 << 20)
     p.add_argument("--n-slots", type=int, default=4)
     p.add_argument("--unit", type=int, default=64 << 10)
-    p.add_argument("--pack", default="lsu", choices=["lsu", "tma"])
+    p.add_argument("--pack", default="lsu", choices=["lsu", "tma", "ce"],
+                   help="pack kernel: 128-bit LSU, TMA bulk through SMEM, or copy engines (zero SMs)")
+    p.add_argument("--gather", default="kernel", choices=["kernel", "ce"],
+                   help="parity: XOR kernel reads peers over NVLink, or copy engines pull units first")
     p.add_argument("--no-corun", action="store_true", help="skip the co-running GEMM measurement")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--cpu-seconds", type=float, default=12.0)
     return p.parse_args()
+
+
+def trace(*a):
+    if os.environ.get("BENCH_TRACE"):
+        print(f"[rank {os.environ.get('RANK', 0)} {time.strftime('%H:%M:%S')}]", *a, file=sys.stderr, flush=True)
 
 
 def env_rank():
@@ -160,6 +168,9 @@ def reference_arm(a, rank, world):
 # ------------------------------------------------------------------ our arm ---------
 def main():
     a = parse()
+    if os.environ.get("BENCH_WATCHDOG_S"):
+        import faulthandler
+        faulthandler.dump_traceback_later(float(os.environ["BENCH_WATCHDOG_S"]), exit=True)
     rank, local, world = env_rank()
     if a.impl == "reference":
         return reference_arm(a, rank, world)
@@ -197,8 +208,10 @@ def main():
         return float(t.item())
 
     specs, ts = make_rank_state(a.config, rank, dev)
+    trace("state ready")
     S = sum(s.nbytes for s in specs)
-    flags = C.CKPT_OPT_TIMING | (C.CKPT_OPT_TMA_PACK if a.pack == "tma" else 0)
+    flags = (C.CKPT_OPT_TIMING | (C.CKPT_OPT_TMA_PACK if a.pack == "tma" else 0)
+             | (C.CKPT_OPT_CE_PACK if a.pack == "ce" else 0) | (C.CKPT_OPT_CE_GATHER if a.gather == "ce" else 0))
     opts = C.ckpt_options_default(n_slots=a.n_slots, bucket_bytes=a.bucket, stripe_unit=a.unit, flags=flags)
     ctx = C.ckpt_create(local, opts)
     t_setup = time.perf_counter()
@@ -210,6 +223,7 @@ def main():
     else:
         C.ckpt_protect(ctx, 1, 0)  # EUNAVAIL: snapshot only, allocates the host arena
     t_setup = time.perf_counter() - t_setup
+    trace("protected", t_setup)
     g = C.ckpt_geometry(ctx)
     m = g["m"]
     stream = torch.cuda.current_stream()
@@ -233,8 +247,9 @@ def main():
         sid = C.ckpt_snapshot(ctx, a.bucket, stream)
         C.ckpt_wait(ctx, sid)
 
-    for _ in range(a.warmup):
+    for i in range(a.warmup):
         step()
+        trace("warmup step", i)
     C.ckpt_stats_reset(ctx)
     barrier()
     torch.cuda.synchronize()
@@ -257,7 +272,7 @@ def main():
     peaks = load_peaks()
     hbm_peak = peaks.get("hbm_gbs", 6650.0)
     kern = []
-    if st["pack_launches"]:
+    if st["pack_launches"] and a.pack != "ce":
         per = st["pack_bytes"] / st["pack_launches"]
         dur = st["pack_ms"] / st["pack_launches"]
         kern.append(("pack", st["pack_ms"], {"bound": "hbm", "achieved": per / dur / 1e6, "peak": hbm_peak,
@@ -265,13 +280,20 @@ def main():
                                              "bytes_per_launch": per, "avg_launch_us": dur * 1e3,
                                              "launches": st["pack_launches"],
                                              "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy r+w)"}))
-    if st["xor_launches"]:
+    if st["xor_launches"] and a.gather == "kernel":
         per = st["xor_bytes_in"] / st["xor_launches"]
         dur = st["xor_ms"] / st["xor_launches"]
         kern.append(("xor", st["xor_ms"], {"bound": "nvlink", "achieved": per / dur / 1e6, "peak": NVLINK_PEAK_GBS,
                                            "unit": "GB/s", "kernel": "xor_kernel<m-1>", "bytes_per_launch": per,
                                            "avg_launch_us": dur * 1e3, "launches": st["xor_launches"],
                                            "peak_source": "B200_PROFILING.md measured peer copy 770 GB/s/direction"}))
+    elif st["xor_launches"]:  # CE gather: the XOR kernel reads local HBM (m-1 streams) and writes parity
+        per = (st["xor_bytes_in"] + st["xor_bytes_out"]) / st["xor_launches"]
+        dur = st["xor_ms"] / st["xor_launches"]
+        kern.append(("xor", st["xor_ms"], {"bound": "hbm", "achieved": per / dur / 1e6, "peak": hbm_peak,
+                                           "unit": "GB/s", "kernel": "xor_kernel<m-1>", "bytes_per_launch": per,
+                                           "avg_launch_us": dur * 1e3, "launches": st["xor_launches"],
+                                           "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy r+w)"}))
     kern.sort(key=lambda x: -x[1])
     roof = kern[0][2] if kern else None
     if roof:
@@ -281,7 +303,7 @@ def main():
         for k in ("achieved", "frac", "avg_launch_us"):
             roof[k] = round(roof[k], 4)
     others = {k: {kk: (round(vv, 4) if isinstance(vv, float) else vv) for kk, vv in d.items()} for k, _, d in kern[1:]}
-    launches = st["pack_launches"] + st["xor_launches"]
+    launches = int(allsum(st["pack_launches"] + st["xor_launches"]))
 
     # co-running bf16 GEMM (the O_in-mem analog, P.234; HAS layer 2, P.423)
     corun = None
@@ -321,14 +343,14 @@ def main():
             "scaling": "weak", "vs_baseline": None, "dtype": "u8", "data": "synthetic",
             "config": {"workload": a.config, "state_bytes_per_gpu": S, "tensors_per_gpu": len(specs),
                        "m": m, "L_star": g["L_star"], "stripe_unit": g["unit"], "bucket_bytes": a.bucket,
-                       "n_slots": a.n_slots, "pack": a.pack,
+                       "n_slots": a.n_slots, "pack": a.pack, "gather": a.gather,
                        "l2": f"inputs {S / 1e9:.2f} GB/GPU >> 126 MB L2; no flush needed"},
             "per_gpu_gbs": round(value / N, 3),
             "host_link": {"achieved_wire_gbs_rank0": round(wire, 3), "peak_d2h_gbs_rank0_measured": round(d2h_peak, 3),
                           "frac": round(wire / d2h_peak, 4),
                           "note": "binding roofline of the whole step: pinned D2H of data + parity"},
             "roofline": roof, "other_kernels": others,
-            "gpu_launches": int(allsum(launches)),
+            "gpu_launches": launches,
             "clocks": clocks,
             "e2e": e2e, "cpu_baseline": cpu, "gemm_corun": corun,
             "setup_s_rank0": round(t_setup, 2),
@@ -363,7 +385,7 @@ def gemm_corun(torch, C, ctx, stream, bucket, barrier, allmax, dev):
     sid = C.ckpt_snapshot(ctx, bucket, stream)
     C.ckpt_wait(ctx, sid)
     snap_ms = C.ckpt_get_stats(ctx)["last_snapshot_ms"] or 250.0
-    iters = int(max(20, 1.5 * snap_ms / per))
+    iters = int(allmax(int(max(20, 1.5 * snap_ms / per))))
 
     def window(with_snap):
         barrier()

@@ -63,6 +63,10 @@ extern "C" {
 #define CKPT_OPT_TIMING      0x1u  /* time every pack/xor launch with CUDA events (stats) */
 #define CKPT_OPT_TMA_PACK    0x2u  /* pack via cp.async.bulk (TMA 1-D) through SMEM       */
 #define CKPT_OPT_LSU_PACK    0x4u  /* force the 128-bit LDG/STG pack                      */
+#define CKPT_OPT_CE_PACK     0x8u  /* pack/unpack with copy-engine D2D copies (zero SMs)  */
+#define CKPT_OPT_CE_GATHER   0x10u /* parity: copy engines pull the m-1 peer units over
+                                      NVLink (2-D copies) into local HBM, then the XOR
+                                      kernel runs locally at HBM speed (few SM-seconds)  */
 
 typedef struct ckpt_options {
     uint32_t struct_size;   /* sizeof(ckpt_options); set by ckpt_options_default       */
@@ -139,6 +143,7 @@ typedef struct ckpt_stats {      /* cumulative since ckpt_stats_reset           
     uint64_t xor_bytes_in;       /* algorithmic: peer bytes read by encode kernels       */
     uint64_t xor_bytes_out;      /* parity bytes written                                 */
     uint64_t d2h_bytes, h2d_bytes;
+    uint64_t ce_copies;          /* copy-engine operations issued (pack/gather/D2H/H2D)  */
     double   pack_ms, xor_ms, unpack_ms, rebuild_ms; /* summed launch durations
                                     (only with CKPT_OPT_TIMING)                          */
     double   last_snapshot_ms;   /* capture event -> last D2H event of the last snapshot

@@ -32,6 +32,8 @@ CKPT_EUNRECOVERABLE = -10
 CKPT_OPT_TIMING = 0x1
 CKPT_OPT_TMA_PACK = 0x2
 CKPT_OPT_LSU_PACK = 0x4
+CKPT_OPT_CE_PACK = 0x8
+CKPT_OPT_CE_GATHER = 0x10
 
 CKPT_DTYPE_BYTES, CKPT_DTYPE_BF16, CKPT_DTYPE_FP16, CKPT_DTYPE_FP32 = 0, 1, 2, 3
 CKPT_ROLE_PARAM, CKPT_ROLE_MASTER, CKPT_ROLE_EXP_AVG, CKPT_ROLE_EXP_AVG_SQ, CKPT_ROLE_OTHER = 0, 1, 2, 3, 4
@@ -70,7 +72,7 @@ class ckpt_group(ctypes.Structure):
 class ckpt_stats(ctypes.Structure):
     _fields_ = [(n, _u64) for n in ("snapshots", "loads", "rebuilds", "pack_launches", "xor_launches",
                                     "unpack_launches", "rebuild_launches", "pack_bytes", "xor_bytes_in",
-                                    "xor_bytes_out", "d2h_bytes", "h2d_bytes")] + \
+                                    "xor_bytes_out", "d2h_bytes", "h2d_bytes", "ce_copies")] + \
                [(n, ctypes.c_double) for n in ("pack_ms", "xor_ms", "unpack_ms", "rebuild_ms", "last_snapshot_ms")]
 
     def as_dict(self):
@@ -149,7 +151,7 @@ def ckpt_strerror(code: int) -> str:
 
 
 def ckpt_last_error() -> str:
-    return lib().ckpt_last_error().decode()
+    return lib().ckpt_last_error().decode(errors="replace")
 
 
 def ckpt_version() -> str:
@@ -314,7 +316,7 @@ def exchange_handles(blob: bytes, group=None) -> bytes:
     assert len(blob) == CKPT_HANDLE_BYTES
     backend = dist.get_backend(group)
     dev = torch.device("cuda", torch.cuda.current_device()) if backend == "nccl" else torch.device("cpu")
-    mine = torch.frombuffer(bytearray(blob), dtype=torch.uint8).to(dev)
+    mine = torch.from_numpy(np.frombuffer(blob, dtype=np.uint8).copy()).to(dev)
     world = dist.get_world_size(group)
     outs = [torch.empty_like(mine) for _ in range(world)]
     dist.all_gather(outs, mine, group=group)

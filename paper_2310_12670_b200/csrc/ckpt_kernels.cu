@@ -122,26 +122,107 @@ __device__ __forceinline__ void block_zero(uint8_t *dst, uint64_t n) {
     if (tid < tail) dst[t0 + tid] = 0;
 }
 
-__global__ void __launch_bounds__(kPackThreads) pack_kernel(const PackArgs a) {
-    for (uint64_t c = blockIdx.x; c < a.count; c += gridDim.x) {
-        const PackChunk ch = a.chunks[a.first + c];
-        const uint64_t lo = ch.dst > a.bucket_begin ? ch.dst : a.bucket_begin;
-        const uint64_t end = ch.dst + ch.nbytes;
-        const uint64_t hi = end < a.bucket_end ? end : a.bucket_end;
-        if (lo >= hi) continue;
-        uint8_t *slot = a.slot + (lo - a.bucket_begin);
-        if (ch.src == 0) {
-            if (!a.unpack) block_zero(slot, hi - lo);
-            continue;
-        }
-        uint8_t *tensor = reinterpret_cast<uint8_t *>(ch.src) + (lo - ch.dst);
-        if (a.unpack)
-            block_copy(tensor, slot, hi - lo);
-        else
-            block_copy(slot, tensor, hi - lo);
-    }
+// This CTA's share of the bucket: tiles split evenly over gridDim.x, then mapped to
+// the contiguous chunk index range [c_begin, c_end).
+__device__ __forceinline__ void cta_chunk_range(const PackArgs &a, uint64_t &c_begin, uint64_t &c_end) {
+    const uint64_t t_lo = a.bucket_begin / kTile;
+    const uint64_t t_hi = (a.bucket_end + kTile - 1) / kTile;
+    const uint64_t nt = t_hi - t_lo, g = gridDim.x, b = blockIdx.x;
+    const uint64_t q = nt / g, r = nt % g;
+    const uint64_t ta = t_lo + b * q + (b < r ? b : r);
+    const uint64_t tb = ta + q + (b < r ? 1 : 0);
+    c_begin = a.tile_first[ta];
+    c_end = a.tile_first[tb];
 }
 
+// Clip chunk c to the bucket; returns bytes (0 = nothing) and the from/to addresses.
+__device__ __forceinline__ uint64_t clip_chunk(const PackArgs &a, const PackChunk &ch, const uint8_t *&from,
+                                               uint8_t *&to) {
+    const uint64_t lo = ch.dst > a.bucket_begin ? ch.dst : a.bucket_begin;
+    const uint64_t end = ch.dst + ch.nbytes;
+    const uint64_t hi = end < a.bucket_end ? end : a.bucket_end;
+    if (lo >= hi) return 0;
+    uint8_t *slot = a.slot + (lo - a.bucket_begin);
+    if (ch.src == 0) {  // zero gap: written on pack, skipped on unpack
+        from = nullptr;
+        to = a.unpack ? nullptr : slot;
+        return a.unpack ? 0 : hi - lo;
+    }
+    uint8_t *tensor = reinterpret_cast<uint8_t *>(ch.src) + (lo - ch.dst);
+    from = a.unpack ? slot : tensor;
+    to = a.unpack ? tensor : slot;
+    return hi - lo;
+}
+
+// LSU pack.  The CTA stages up to kBatch chunk descriptors in SMEM, then streams the
+// 16-byte words of all 16-B-aligned chunks of the batch as ONE flat index space, so
+// every thread keeps kPackUnroll independent 128-bit loads in flight across chunk
+// boundaries (chunks are <= 16 KiB).  Unaligned chunks (views misaligned mod 16,
+// odd-sized tails, small gaps) take the block-cooperative funnel-shift path.
+constexpr int kBatch = 128;
+
+__global__ void __launch_bounds__(kPackThreads) pack_kernel(const PackArgs a) {
+    __shared__ const uint8_t *s_from[kBatch];
+    __shared__ uint8_t *s_to[kBatch];
+    __shared__ uint64_t s_n[kBatch];
+    __shared__ uint32_t s_pre[kBatch + 1];
+    __shared__ uint32_t s_nslow;
+    __shared__ uint8_t s_slow[kBatch];
+    uint64_t cb, ce;
+    cta_chunk_range(a, cb, ce);
+    const uint32_t tid = threadIdx.x, nt = blockDim.x;
+    for (uint64_t c0 = cb; c0 < ce; c0 += kBatch) {
+        const uint32_t nb = (uint32_t)((ce - c0) < kBatch ? (ce - c0) : kBatch);
+        if (tid == 0) s_nslow = 0;
+        __syncthreads();
+        if (tid < nb) {
+            const uint8_t *from;
+            uint8_t *to;
+            const uint64_t n = clip_chunk(a, a.chunks[c0 + tid], from, to);
+            const bool vec = n && ((((uintptr_t)from | (uintptr_t)to | n) & 15) == 0);
+            s_from[tid] = from;
+            s_to[tid] = to;
+            s_n[tid] = n;
+            s_pre[tid + 1] = vec ? (uint32_t)(n >> 4) : 0;
+            if (n && !vec) s_slow[atomicAdd(&s_nslow, 1u)] = (uint8_t)tid;
+        }
+        __syncthreads();
+        if (tid == 0) {
+            s_pre[0] = 0;
+            for (uint32_t i = 1; i <= nb; ++i) s_pre[i] += s_pre[i - 1];
+        }
+        __syncthreads();
+        const uint32_t total = s_pre[nb];
+        uint32_t k = 0;  // per-thread chunk cursor (word indices only grow)
+        for (uint32_t base = 0; base < total; base += nt * kPackUnroll) {
+            uint4 v[kPackUnroll];
+            uint4 *dst[kPackUnroll];
+#pragma unroll
+            for (int u = 0; u < kPackUnroll; ++u) {
+                const uint32_t w = base + u * nt + tid;
+                dst[u] = nullptr;
+                if (w < total) {
+                    while (s_pre[k + 1] <= w) ++k;
+                    const uint32_t off = w - s_pre[k];
+                    const uint8_t *f = s_from[k];
+                    dst[u] = reinterpret_cast<uint4 *>(s_to[k]) + off;
+                    v[u] = f ? ld_stream(reinterpret_cast<const uint4 *>(f) + off) : make_uint4(0, 0, 0, 0);
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < kPackUnroll; ++u)
+                if (dst[u]) st_stream(dst[u], v[u]);
+        }
+        for (uint32_t i = 0; i < s_nslow; ++i) {
+            const uint32_t j = s_slow[i];
+            if (s_from[j])
+                block_copy(s_to[j], s_from[j], s_n[j]);
+            else
+                block_zero(s_to[j], s_n[j]);
+        }
+        __syncthreads();
+    }
+}
 
 // ---------------------------------------------------------------------------------
 // TMA pack: 1-D bulk copies (cp.async.bulk) global -> SMEM -> global issued by one
@@ -217,21 +298,17 @@ __global__ void __launch_bounds__(kTmaThreads) pack_tma_kernel(const PackArgs a)
     uint32_t phase = 0;      // bit i = parity to wait for on stage i
     uint32_t issued = 0, done = 0;  // pieces loaded / stored (lane 0 only)
     Piece ring[kTmaStages];
-    for (uint64_t c = blockIdx.x; c < a.count; c += gridDim.x) {
-        const PackChunk ch = a.chunks[a.first + c];
-        const uint64_t lo = ch.dst > a.bucket_begin ? ch.dst : a.bucket_begin;
-        const uint64_t end = ch.dst + ch.nbytes;
-        const uint64_t hi = end < a.bucket_end ? end : a.bucket_end;
-        if (lo >= hi) continue;
-        uint8_t *slot = a.slot + (lo - a.bucket_begin);
-        uint64_t n = hi - lo;
-        if (ch.src == 0) {
-            if (!a.unpack) block_zero(slot, n);
+    uint64_t cb, ce;
+    cta_chunk_range(a, cb, ce);
+    for (uint64_t c = cb; c < ce; ++c) {
+        const uint8_t *src;
+        uint8_t *dst;
+        const uint64_t n = clip_chunk(a, a.chunks[c], src, dst);
+        if (n == 0) continue;
+        if (!src) {
+            block_zero(dst, n);
             continue;
         }
-        uint8_t *tensor = reinterpret_cast<uint8_t *>(ch.src) + (lo - ch.dst);
-        uint8_t *dst = a.unpack ? tensor : slot;
-        const uint8_t *src = a.unpack ? slot : tensor;
         if ((((uintptr_t)dst ^ (uintptr_t)src) & 15) || n < 64) {
             block_copy(dst, src, n);
             continue;
@@ -334,10 +411,21 @@ cudaError_t launch_xor_n(const XorArgs &a, int grid, cudaStream_t s) {
     return cudaGetLastError();
 }
 
+__global__ void signal_kernel(const SignalArgs a) {
+    const int i = threadIdx.x;
+    if (i < a.n) asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(a.addr[i]), "r"(a.value) : "memory");
+}
+
 }  // namespace
 
-cudaError_t launch_pack(const PackArgs &a, int grid, cudaStream_t s, bool tma) {
-    if (a.count == 0) return cudaSuccess;
+cudaError_t launch_signal(const SignalArgs &a, cudaStream_t s) {
+    signal_kernel<<<1, 32, 0, s>>>(a);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_pack(const PackArgs &a, int max_ctas, cudaStream_t s, bool tma) {
+    if (a.bucket_end <= a.bucket_begin) return cudaSuccess;
+    const uint64_t ntiles = (a.bucket_end + kTile - 1) / kTile - a.bucket_begin / kTile;
     if (tma) {
         static bool attr_set = false;  // per process; the attribute is per function
         const int smem = kTmaStages * kTmaStage;
@@ -346,12 +434,13 @@ cudaError_t launch_pack(const PackArgs &a, int grid, cudaStream_t s, bool tma) {
             if (e != cudaSuccess) return e;
             attr_set = true;
         }
-        // 3 CTAs of 64 KiB SMEM per SM
-        uint64_t g = a.count < (uint64_t)grid * 3 / 2 ? a.count : (uint64_t)grid * 3 / 2;
+        // 3 CTAs of 64 KiB SMEM per SM: 1.5x the LSU CTA budget
+        const uint64_t cap = (uint64_t)max_ctas * 3 / 2;
+        const uint64_t g = ntiles < cap ? ntiles : cap;
         pack_tma_kernel<<<(unsigned)g, kTmaThreads, smem, s>>>(a);
         return cudaGetLastError();
     }
-    uint64_t g = a.count < (uint64_t)grid ? a.count : (uint64_t)grid;
+    const uint64_t g = ntiles < (uint64_t)max_ctas ? ntiles : (uint64_t)max_ctas;
     pack_kernel<<<(unsigned)g, kPackThreads, 0, s>>>(a);
     return cudaGetLastError();
 }

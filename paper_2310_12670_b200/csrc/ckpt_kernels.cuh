@@ -16,12 +16,17 @@ struct PackChunk {
     uint64_t seg;
 };
 
-// Pack (tensors -> slot) or unpack (slot -> tensors) of the chunks [first, first+count)
-// clipped to the bucket's image range [bucket_begin, bucket_end).  The slot holds
-// image byte bucket_begin at address slot.
+// Image tiles: the planner cuts every chunk (data and zero) at multiples of kTile
+// bytes of image, so the chunks of tile i are exactly [tile_first[i], tile_first[i+1]).
+// A launch splits the bucket's tiles evenly over its CTAs (balanced by bytes).
+constexpr uint64_t kTile = 16 * 1024;
+
+// Pack (tensors -> slot) or unpack (slot -> tensors) of the bucket's image range
+// [bucket_begin, bucket_end) (clipped to the rank's L).  The slot holds image byte
+// bucket_begin at address slot.
 struct PackArgs {
     const PackChunk *chunks;
-    uint64_t first, count;
+    const uint32_t *tile_first;
     uint64_t bucket_begin, bucket_end;
     uint8_t *slot;
     int unpack;
@@ -55,8 +60,17 @@ struct XorArgs {
     uint64_t unit;
 };
 
+// Cross-rank signal by a one-warp kernel: st.release.sys of `value` to every address
+// (peers' IPC-mapped flag words).  Alternative to cuStreamWriteValue32 (CKPT_SIGNAL=kernel).
+struct SignalArgs {
+    uint32_t *addr[kMaxTerms];
+    int n;
+    uint32_t value;
+};
+
 // Launchers (return the cudaError_t of the launch).
-cudaError_t launch_pack(const PackArgs &a, int grid, cudaStream_t s, bool tma);
+cudaError_t launch_signal(const SignalArgs &a, cudaStream_t s);
+cudaError_t launch_pack(const PackArgs &a, int max_ctas, cudaStream_t s, bool tma);
 cudaError_t launch_xor(const XorArgs &a, int max_ctas, cudaStream_t s);
 
 }  // namespace reft

@@ -83,7 +83,6 @@ static int load_memops() {
 namespace {
 constexpr uint32_t kMagic = 0x52454654u;  // "REFT"
 constexpr uint32_t kAbiVersion = 1;
-constexpr uint64_t kChunk = 64 * 1024;  // pack work item (bytes of image)
 // flag page: 3 arrays of CKPT_MAX_GROUP uint32, each on its own 128-B line
 enum Stage { kReady = 0, kRel = 1, kDone = 2, kNumStages = 3 };
 constexpr uint64_t kFlagStride = 32;  // uint32 per stage line
@@ -140,6 +139,8 @@ struct ckpt_ctx {
     uint64_t L = 0;  // L_j
     std::vector<PackChunk> chunks;
     PackChunk *d_chunks = nullptr;
+    const uint32_t *d_tile_first = nullptr;  // inside the d_chunks allocation
+    std::vector<uint32_t> tile_first;        // host copy (CE pack)
     ckpt_layout layout{};
 
     // device staging (exported)
@@ -160,6 +161,9 @@ struct ckpt_ctx {
     bool peer_opened[CKPT_MAX_GROUP] = {};
     ckpt_ctx *members[CKPT_MAX_GROUP] = {};
 
+    // CE gather buffer (CKPT_OPT_CE_GATHER; local): m-1 unit streams per bucket
+    uint8_t *gather = nullptr;
+    uint64_t gather_bytes = 0;
     // parity (local, not exported)
     uint8_t *parity = nullptr;
     uint64_t parity_bytes = 0, parity_slot_bytes = 0;
@@ -168,13 +172,14 @@ struct ckpt_ctx {
     HostBuf hdata[2], hpar[2];
     int nbuf = 2;
     int completed = -1, ongoing = 0;
+    bool pad_dirty[2] = {false, false};  // zero pad [L, L*) overwritten by ckpt_forget
     uint64_t completed_id = 0;
 
     // streams / events
-    cudaStream_t sP = nullptr, sX = nullptr, sC = nullptr, sW = nullptr;
+    cudaStream_t sP = nullptr, sX = nullptr, sC = nullptr, sW = nullptr, sG = nullptr;
     cudaEvent_t ev_capture = nullptr, ev_pack_all = nullptr, ev_done = nullptr, ev_t0 = nullptr,
                 ev_t1 = nullptr;
-    std::vector<cudaEvent_t> ev_packed, ev_xored, ev_d2h_data, ev_d2h_par, ev_h2d, ev_kdone;
+    std::vector<cudaEvent_t> ev_packed, ev_xored, ev_d2h_data, ev_d2h_par, ev_h2d, ev_kdone, ev_gathered;
     // LOCAL transport: per-stage per-slot signal events
     std::vector<cudaEvent_t> ev_sig[kNumStages];
 
@@ -413,7 +418,7 @@ extern "C" int ckpt_create(int device, const ckpt_options *o, ckpt_ctx **out) {
     int prio = opt.priority == INT32_MAX ? least : std::min(least, std::max(greatest, (int)opt.priority));
     c->opt.priority = prio;
     cudaError_t e = cudaSuccess;
-    cudaStream_t *ss[4] = {&c->sP, &c->sX, &c->sC, &c->sW};
+    cudaStream_t *ss[5] = {&c->sP, &c->sX, &c->sC, &c->sW, &c->sG};
     for (auto s : ss)
         if (e == cudaSuccess) e = cudaStreamCreateWithPriority(s, cudaStreamNonBlocking, prio);
     cudaEvent_t *es[3] = {&c->ev_capture, &c->ev_pack_all, &c->ev_done};
@@ -432,7 +437,7 @@ extern "C" int ckpt_create(int device, const ckpt_options *o, ckpt_ctx **out) {
 extern "C" int ckpt_destroy(ckpt_ctx *c) {
     if (!c) return CKPT_OK;
     cudaSetDevice(c->device);
-    cudaStream_t ss[4] = {c->sP, c->sX, c->sC, c->sW};
+    cudaStream_t ss[5] = {c->sP, c->sX, c->sC, c->sW, c->sG};
     for (auto s : ss)
         if (s) cudaStreamSynchronize(s);
     for (uint32_t j = 0; j < CKPT_MAX_GROUP; ++j) {
@@ -452,6 +457,7 @@ extern "C" int ckpt_destroy(ckpt_ctx *c) {
     destroy_events(c->ev_d2h_par);
     destroy_events(c->ev_h2d);
     destroy_events(c->ev_kdone);
+    destroy_events(c->ev_gathered);
     for (auto &v : c->ev_sig) destroy_events(v);
     for (auto &t : c->timed) {
         cudaEventDestroy(t.a);
@@ -461,6 +467,7 @@ extern "C" int ckpt_destroy(ckpt_ctx *c) {
     if (c->staging) cudaFree(c->staging);
     if (c->flags) cudaFree(c->flags);
     if (c->parity) cudaFree(c->parity);
+    if (c->gather) cudaFree(c->gather);
     for (int i = 0; i < 2; ++i) {
         host_free(c->hdata[i]);
         host_free(c->hpar[i]);
@@ -488,35 +495,49 @@ extern "C" int ckpt_register(ckpt_ctx *c, const ckpt_tensor *t, uint64_t n, cons
         segs[i] = Segment{(uint64_t)(uintptr_t)t[i].dev_ptr, t[i].nbytes, 0, t[i].dtype, t[i].role, t[i].flags,
                           t[i].name ? t[i].name : ""};
     }
-    // plan (reading Q6): registration order, A-aligned offsets, zero gaps
+    // plan (reading Q6): registration order, A-aligned offsets, zero gaps.  Every
+    // piece (data or zero gap) is cut at multiples of kTile bytes of image so that the
+    // chunks of image tile i are exactly [tile_first[i], tile_first[i+1]).
     uint64_t end = 0;
     std::vector<PackChunk> ch;
-    for (uint64_t i = 0; i < n; ++i) {
-        uint64_t off = align_up(end, c->opt.align);
-        if (off > end) ch.push_back(PackChunk{0, end, off - end, i});  // zero gap
-        segs[i].off = off;
-        for (uint64_t o = 0; o < segs[i].nbytes;) {
-            // cut at image offsets that are multiples of kChunk so buckets split cleanly
-            uint64_t img = off + o;
-            uint64_t lim = std::min(segs[i].nbytes - o, align_up(img + 1, kChunk) - img);
-            ch.push_back(PackChunk{segs[i].dev + o, img, lim, i});
+    auto emit = [&ch](uint64_t src, uint64_t img, uint64_t nbytes, uint64_t seg) {
+        for (uint64_t o = 0; o < nbytes;) {
+            const uint64_t at = img + o;
+            const uint64_t lim = std::min(nbytes - o, align_up(at + 1, kTile) - at);
+            ch.push_back(PackChunk{src ? src + o : 0, at, lim, seg});
             o += lim;
         }
+    };
+    for (uint64_t i = 0; i < n; ++i) {
+        uint64_t off = align_up(end, c->opt.align);
+        if (off > end) emit(0, end, off - end, i);  // zero gap
+        segs[i].off = off;
+        emit(segs[i].dev, off, segs[i].nbytes, i);
         end = off + segs[i].nbytes;
     }
     uint64_t L = align_up(end, c->opt.align);
-    if (L > end) ch.push_back(PackChunk{0, end, L - end, n});
+    if (L > end) emit(0, end, L - end, n);
+    if (ch.size() >= (1ull << 32)) return fail(CKPT_EINVAL, "register: state too large (chunk index overflow)");
+    const uint64_t ntiles = (L + kTile - 1) / kTile;
+    std::vector<uint32_t> tf(ntiles + 1);
+    for (uint64_t t = 0, ci = 0; t <= ntiles; ++t) {
+        while (ci < ch.size() && ch[ci].dst < t * kTile) ++ci;
+        tf[t] = (uint32_t)ci;
+    }
     // device staging: full image (n_slots == 0) or a ring of n_slots buckets
     c->full_copy = c->opt.n_slots == 0;
     c->n_slots = c->opt.n_slots;
     c->slot_bytes = align_up(c->opt.bucket_bytes, 4096);
     c->staging_bytes = c->full_copy ? std::max<uint64_t>(L, 4096) : (uint64_t)c->n_slots * c->slot_bytes;
     PackChunk *dch = nullptr;
-    if (cudaMalloc(&dch, ch.size() * sizeof(PackChunk)) != cudaSuccess) {
+    const uint64_t tbytes = ch.size() * sizeof(PackChunk), fbytes = tf.size() * sizeof(uint32_t);
+    if (cudaMalloc(&dch, tbytes + fbytes) != cudaSuccess) {
         cudaGetLastError();
         return fail(CKPT_ENOMEM, "register: chunk table allocation failed");
     }
-    CUDA_TRY(cudaMemcpy(dch, ch.data(), ch.size() * sizeof(PackChunk), cudaMemcpyHostToDevice));
+    CUDA_TRY(cudaMemcpy(dch, ch.data(), tbytes, cudaMemcpyHostToDevice));
+    CUDA_TRY(cudaMemcpy((uint8_t *)dch + tbytes, tf.data(), fbytes, cudaMemcpyHostToDevice));
+    c->d_tile_first = (const uint32_t *)((uint8_t *)dch + tbytes);
     if (cudaMalloc(&c->staging, c->staging_bytes) != cudaSuccess ||
         cudaMalloc(&c->flags, kFlagBytes) != cudaSuccess) {
         cudaGetLastError();
@@ -528,6 +549,7 @@ extern "C" int ckpt_register(ckpt_ctx *c, const ckpt_tensor *t, uint64_t n, cons
     CUDA_TRY(cudaMemset(c->flags, 0, kFlagBytes));
     CUDA_TRY(cudaMemset(c->staging, 0, c->staging_bytes));
     c->d_chunks = dch;
+    c->tile_first = std::move(tf);
     c->chunks = std::move(ch);
     c->segs = std::move(segs);
     c->L = L;
@@ -631,15 +653,17 @@ extern "C" int ckpt_protect(ckpt_ctx *c, const ckpt_group *g) {
         if (!g->handles) return fail(CKPT_EINVAL, "protect: IPC group without handles");
         if (load_memops()) return fail(CKPT_ECUDA, "protect: stream memory operations unavailable");
         const HandleBlob *hb[CKPT_MAX_GROUP];
-        for (uint32_t j = 0; j < m; ++j) {
+        for (uint32_t j = 0; j < m; ++j)
             hb[j] = (const HandleBlob *)((const uint8_t *)g->handles + (uint64_t)j * CKPT_HANDLE_BYTES);
+        for (uint32_t j = 0; j < m; ++j) {
             if (hb[j]->magic != kMagic || hb[j]->version != kAbiVersion)
                 return fail(CKPT_EINVAL, "protect: handle %u is not a reft-ckpt v%u blob", j, kAbiVersion);
             if (hb[j]->align != c->opt.align || hb[j]->unit != c->opt.stripe_unit ||
                 hb[j]->slot_bytes != c->slot_bytes || hb[j]->n_slots != c->n_slots || hb[j]->full_copy != (uint32_t)c->full_copy)
                 return fail(CKPT_EMISMATCH, "protect: member %u geometry differs (align/unit/slots)", j);
             if (strncmp(hb[j]->host, hb[g->my_index]->host, sizeof hb[j]->host) != 0)
-                return fail(CKPT_EMISMATCH, "protect: member %u is on another host (node group only, Q1)", j);
+                return fail(CKPT_EMISMATCH, "protect: member %u is on another host '%.64s' vs '%.64s' (node group only, Q1)",
+                            j, hb[j]->host, hb[g->my_index]->host);
             Ls[j] = hb[j]->L;
         }
         if (hb[g->my_index]->pid != (int32_t)getpid() || hb[g->my_index]->L != c->L)
@@ -721,6 +745,13 @@ extern "C" int ckpt_protect(ckpt_ctx *c, const ckpt_group *g) {
         cudaGetLastError();
         return fail(CKPT_ENOMEM, "protect: parity buffer of %llu bytes failed", (unsigned long long)c->parity_bytes);
     }
+    if (c->opt.flags & CKPT_OPT_CE_GATHER) {
+        c->gather_bytes = c->full_copy ? std::max<uint64_t>(Lstar, 4096) : c->parity_bytes * (m - 1);
+        if (cudaMalloc(&c->gather, c->gather_bytes) != cudaSuccess) {
+            cudaGetLastError();
+            return fail(CKPT_ENOMEM, "protect: CE gather buffer of %llu bytes failed", (unsigned long long)c->gather_bytes);
+        }
+    }
     rc = alloc_arena(c);
     if (rc) return rc;
     c->seq = 0;
@@ -746,10 +777,31 @@ static inline uint32_t bucket_seq(const ckpt_ctx *c, uint64_t k) { return c->op_
 static inline bool ring_reuse(const ckpt_ctx *c, uint64_t k) { return !c->full_copy && k >= c->n_slots; }
 
 // ------------------------------------------------------------------ signals ---------
+// IPC signals: cuStreamWriteValue32 into the peer's flag page (default, zero SMs) or a
+// one-warp st.release.sys kernel (CKPT_SIGNAL=kernel).  Waits are always
+// cuStreamWaitValue32 on the local flag page.
+static bool signal_by_kernel() {
+    static int v = -1;
+    if (v < 0) {
+        const char *e = getenv("CKPT_SIGNAL");
+        v = (e && strcmp(e, "kernel") == 0) ? 1 : 0;
+    }
+    return v == 1;
+}
+
 // signal(stage, seq): tell every other member that this member reached `seq`.
 static int sig_signal(ckpt_ctx *c, cudaStream_t s, int stage, uint32_t seq, uint32_t slot) {
     if (c->m < 2) return CKPT_OK;
     if (c->transport == CKPT_GROUP_IPC) {
+        if (signal_by_kernel()) {
+            SignalArgs a;
+            memset(&a, 0, sizeof a);
+            for (uint32_t j = 0; j < c->m; ++j)
+                if (j != c->me) a.addr[a.n++] = c->peer_flags[j] + stage * kFlagStride + c->me;
+            a.value = seq;
+            CUDA_TRY(launch_signal(a, s));
+            return CKPT_OK;
+        }
         for (uint32_t j = 0; j < c->m; ++j) {
             if (j == c->me) continue;
             CUdeviceptr a = (CUdeviceptr)(uintptr_t)(c->peer_flags[j] + stage * kFlagStride + c->me);
@@ -788,17 +840,46 @@ static int wait_all(ckpt_ctx *c, cudaStream_t s, int stage, uint32_t seq, uint32
 }
 
 // ------------------------------------------------------------------ kernels ---------
+// Copy-engine pack/unpack (CKPT_OPT_CE_PACK): one D2D cudaMemcpyAsync per contiguous
+// piece of a tensor inside the bucket; zero SMs.  Gaps must read as zero: the full
+// staging image was zeroed at registration and gaps are never written; a ring slot is
+// cleared with one memset before its copies.
+static int do_pack_ce(ckpt_ctx *c, uint64_t k, uint8_t *slot, cudaStream_t s, bool unpack) {
+    const uint64_t bb = bucket_begin(c, k), be = std::min(bucket_end(c, k), c->L);
+    const uint64_t t_lo = bb / kTile, t_hi = (be + kTile - 1) / kTile;
+    uint64_t ci = c->tile_first[t_lo], ce = c->tile_first[t_hi];
+    if (!unpack && !c->full_copy) {
+        CUDA_TRY(cudaMemsetAsync(slot, 0, be - bb, s));
+        c->st.ce_copies++;
+    }
+    while (ci < ce) {
+        const PackChunk &a = c->chunks[ci];
+        uint64_t cj = ci + 1;  // merge the contiguous pieces of one tensor
+        while (cj < ce && c->chunks[cj].seg == a.seg && c->chunks[cj].src != 0 && a.src != 0) ++cj;
+        const PackChunk &z = c->chunks[cj - 1];
+        ci = cj;
+        if (a.src == 0) continue;
+        const uint64_t lo = std::max(a.dst, bb), hi = std::min(z.dst + z.nbytes, be);
+        if (lo >= hi) continue;
+        uint8_t *tensor = (uint8_t *)(uintptr_t)(a.src + (lo - a.dst));
+        uint8_t *sl = slot + (lo - bb);
+        CUDA_TRY(cudaMemcpyAsync(unpack ? tensor : sl, unpack ? sl : tensor, hi - lo, cudaMemcpyDeviceToDevice, s));
+        c->st.ce_copies++;
+    }
+    if (unpack)
+        c->st.unpack_launches += 0;
+    else
+        c->st.pack_bytes += 2 * (be - bb);
+    return CKPT_OK;
+}
+
 static int do_pack(ckpt_ctx *c, uint64_t k, uint8_t *slot, cudaStream_t s, bool unpack) {
     const uint64_t bb = bucket_begin(c, k), be = std::min(bucket_end(c, k), c->L);
     if (be <= bb) return CKPT_OK;
-    // chunk range overlapping [bb, be): chunks sorted by dst and contiguous
-    auto lo = std::upper_bound(c->chunks.begin(), c->chunks.end(), bb,
-                               [](uint64_t v, const PackChunk &x) { return v < x.dst + x.nbytes; });
-    auto hi = std::lower_bound(lo, c->chunks.end(), be, [](const PackChunk &x, uint64_t v) { return x.dst < v; });
+    if (c->opt.flags & CKPT_OPT_CE_PACK) return do_pack_ce(c, k, slot, s, unpack);
     PackArgs a;
     a.chunks = c->d_chunks;
-    a.first = (uint64_t)(lo - c->chunks.begin());
-    a.count = (uint64_t)(hi - lo);
+    a.tile_first = c->d_tile_first;
     a.bucket_begin = bb;
     a.bucket_end = be;
     a.slot = slot;
@@ -889,6 +970,14 @@ static int do_rebuild_row(ckpt_ctx *c, uint64_t k, uint32_t kl, cudaStream_t s) 
 }
 
 // ------------------------------------------------------------------ snapshot --------
+// The image's zero pad [L, L*) is structural (Q5) and never written by a D2H (which
+// covers [0, L)); after ckpt_forget poisoned a buffer, re-zero it before it commits.
+static void clean_pad(ckpt_ctx *c, int buf) {
+    if (buf < 0 || !c->pad_dirty[buf]) return;
+    if (c->Lstar > c->L) memset(c->hdata[buf].p + c->L, 0, c->Lstar - c->L);
+    c->pad_dirty[buf] = false;
+}
+
 static int check_sticky(ckpt_ctx *c) {
     if (c->sticky) return fail(c->sticky, "context has a sticky error: %s", c->sticky_msg.c_str());
     return CKPT_OK;
@@ -919,7 +1008,8 @@ static int prepare_op(ckpt_ctx *c, uint64_t B) {
     c->seq += (uint32_t)c->op_NB + 1;
     const size_t ne = c->full_copy ? (size_t)std::max<uint64_t>(c->op_NB, 1) : c->n_slots;
     int rc = 0;
-    for (auto *v : {&c->ev_packed, &c->ev_xored, &c->ev_d2h_data, &c->ev_d2h_par, &c->ev_h2d, &c->ev_kdone})
+    for (auto *v : {&c->ev_packed, &c->ev_xored, &c->ev_d2h_data, &c->ev_d2h_par, &c->ev_h2d, &c->ev_kdone,
+                    &c->ev_gathered})
         if (!rc) rc = ensure_events(*v, ne);
     return rc;
 }
@@ -938,11 +1028,97 @@ static int stage_pack(ckpt_ctx *c, uint64_t k) {
     return CKPT_OK;
 }
 
+// CE gather (CKPT_OPT_CE_GATHER): copy engines pull unit sigma(me, j) of every stripe
+// of peer j's slot (a 2-D copy: width u, source pitch (m-1)u) into local stream jj;
+// bytes beyond the peer's L_j are zero-filled (Q5).  Zero SMs on NVLink.
+static inline uint64_t gather_stride(const ckpt_ctx *c, uint64_t k) {
+    return c->full_copy ? (bucket_end(c, k) - bucket_begin(c, k)) / (c->m - 1) : c->parity_slot_bytes;
+}
+static inline uint8_t *gather_slot_ptr(const ckpt_ctx *c, uint64_t k) {
+    return c->full_copy ? c->gather + bucket_begin(c, k)
+                        : c->gather + (uint64_t)(k % c->n_slots) * c->parity_slot_bytes * (c->m - 1);
+}
+
+static int do_gather_ce(ckpt_ctx *c, uint64_t k, cudaStream_t s) {
+    const uint64_t bb = bucket_begin(c, k), be = bucket_end(c, k);
+    const uint64_t u = c->unit, pitch = (uint64_t)(c->m - 1) * u, nst = (be - bb) / pitch;
+    const uint64_t gs = gather_stride(c, k);
+    uint8_t *g = gather_slot_ptr(c, k);
+    uint32_t jj = 0;
+    for (uint32_t j = 0; j < c->m; ++j) {
+        if (j == c->me) continue;
+        uint8_t *dst = g + (uint64_t)jj++ * gs;
+        const uint8_t *src = slot_ptr(c, c->peer_staging[j], k);
+        const uint64_t v = valid_in_bucket(c->peer_L[j], bb, be), off = (uint64_t)sigma(c->me, j) * u;
+        const uint64_t full = v >= off + u ? std::min(nst, (v - off - u) / pitch + 1) : 0;
+        if (full == 1 || (full && nst == 1)) {
+            CUDA_TRY(cudaMemcpyAsync(dst, src + off, u, cudaMemcpyDeviceToDevice, s));
+        } else if (full) {
+            CUDA_TRY(cudaMemcpy2DAsync(dst, u, src + off, pitch, u, full, cudaMemcpyDeviceToDevice, s));
+        }
+        uint64_t done = full * u;
+        if (full < nst) {
+            const uint64_t start = full * pitch + off;
+            if (v > start) {
+                CUDA_TRY(cudaMemcpyAsync(dst + done, src + start, v - start, cudaMemcpyDeviceToDevice, s));
+                done += v - start;
+                c->st.ce_copies++;
+            }
+            CUDA_TRY(cudaMemsetAsync(dst + done, 0, nst * u - done, s));
+            c->st.ce_copies++;
+        }
+        if (full) c->st.ce_copies++;
+        c->st.xor_bytes_in += (be - bb) / (c->m - 1);
+    }
+    return CKPT_OK;
+}
+
+static int do_encode_gathered(ckpt_ctx *c, uint64_t k, cudaStream_t s) {
+    const uint64_t bb = bucket_begin(c, k), be = bucket_end(c, k);
+    const uint64_t gs = gather_stride(c, k);
+    XorArgs a;
+    memset(&a, 0, sizeof a);
+    for (uint32_t jj = 0; jj + 1 < c->m; ++jj) {
+        XorTerm &t = a.in[a.nin++];
+        t.base = gather_slot_ptr(c, k) + (uint64_t)jj * gs;
+        t.valid = UINT64_MAX;
+        t.stride = c->unit;
+        t.off = 0;
+    }
+    a.out = parity_slot_ptr(c, k);
+    a.out_valid = UINT64_MAX;
+    a.out_stride = c->unit;
+    a.out_off = 0;
+    a.nstripes = (be - bb) / ((uint64_t)(c->m - 1) * c->unit);
+    a.unit = c->unit;
+    TimedLaunch *t;
+    int rc = timed_begin(c, s, 1, &t);
+    if (rc) return rc;
+    CUDA_TRY(launch_xor(a, c->max_ctas, s));
+    rc = timed_end(t, s);
+    if (rc) return rc;
+    c->st.xor_launches++;
+    c->st.xor_bytes_out += (be - bb) / (c->m - 1);
+    return CKPT_OK;
+}
+
 // Stage 2: parity of bucket k once every member's pack(k) is visible, then REL.
 static int stage_xor(ckpt_ctx *c, uint64_t k) {
     if (c->m < 2) return CKPT_OK;
     const uint32_t s = slot_of(c, k);
     int rc;
+    if (c->opt.flags & CKPT_OPT_CE_GATHER) {
+        if ((rc = wait_all(c, c->sG, kReady, bucket_seq(c, k), s))) return rc;
+        if (ring_reuse(c, k)) CUDA_TRY(cudaStreamWaitEvent(c->sG, c->ev_xored[s], 0));
+        if ((rc = do_gather_ce(c, k, c->sG))) return rc;
+        CUDA_TRY(cudaEventRecord(c->ev_gathered[s], c->sG));
+        if ((rc = sig_signal(c, c->sG, kRel, bucket_seq(c, k), s))) return rc;
+        CUDA_TRY(cudaStreamWaitEvent(c->sX, c->ev_gathered[s], 0));
+        if (ring_reuse(c, k)) CUDA_TRY(cudaStreamWaitEvent(c->sX, c->ev_d2h_par[s], 0));
+        if ((rc = do_encode_gathered(c, k, c->sX))) return rc;
+        CUDA_TRY(cudaEventRecord(c->ev_xored[s], c->sX));
+        return CKPT_OK;
+    }
     CUDA_TRY(cudaStreamWaitEvent(c->sX, c->ev_packed[s], 0));
     if ((rc = wait_all(c, c->sX, kReady, bucket_seq(c, k), s))) return rc;
     if (ring_reuse(c, k)) CUDA_TRY(cudaStreamWaitEvent(c->sX, c->ev_d2h_par[s], 0));
@@ -1088,9 +1264,25 @@ static int sync_stream_timeout(ckpt_ctx *c, cudaStream_t s, const char *what) {
         if (e != cudaErrorNotReady) return fail(CKPT_ECUDA, "%s: %s", what, cudaGetErrorString(e));
         double el = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
         if (el > limit) {
-            // release our own stream waits so the context can be destroyed
+            // snapshot of the flag page for the message, then release our own stream
+            // waits so the context can be destroyed
+            uint32_t f[kNumStages * kFlagStride] = {};
+            cudaStream_t t = nullptr;
+            if (c->flags && cudaStreamCreateWithFlags(&t, cudaStreamNonBlocking) == cudaSuccess) {
+                cudaMemcpyAsync(f, c->flags, sizeof f, cudaMemcpyDeviceToHost, t);
+                cudaStreamSynchronize(t);
+                cudaStreamDestroy(t);
+            }
+            char buf[512];
+            int o = snprintf(buf, sizeof buf, "seq_base=%u NB=%llu", c->op_seq_base, (unsigned long long)c->op_NB);
+            for (int st = 0; st < kNumStages && o < (int)sizeof buf; ++st) {
+                o += snprintf(buf + o, sizeof buf - o, " %s=[", st == 0 ? "READY" : st == 1 ? "REL" : "DONE");
+                for (uint32_t j = 0; j < c->m && o < (int)sizeof buf; ++j)
+                    o += snprintf(buf + o, sizeof buf - o, "%u%s", f[st * kFlagStride + j], j + 1 < c->m ? "," : "]");
+            }
             cudaMemset(c->flags, 0x7f, kFlagBytes);
-            return fail(CKPT_EPEER, "%s: timed out after %.0f s waiting for peers", what, limit);
+            cudaGetLastError();
+            return fail(CKPT_EPEER, "%s: timed out after %.0f s waiting for peers (member %u: %s)", what, limit, c->me, buf);
         }
         std::this_thread::sleep_for(std::chrono::microseconds(el < 0.01 ? 20 : 200));
     }
@@ -1098,7 +1290,7 @@ static int sync_stream_timeout(ckpt_ctx *c, cudaStream_t s, const char *what) {
 
 static int wait_done_all(ckpt_ctx *c, uint32_t done_seq) {
     int rc;
-    cudaStream_t ss[3] = {c->sP, c->sX, c->sC};
+    cudaStream_t ss[4] = {c->sP, c->sX, c->sC, c->sG};
     for (auto s : ss)
         if ((rc = sync_stream_timeout(c, s, "wait"))) return rc;
     if (c->m >= 2) {
@@ -1137,6 +1329,7 @@ extern "C" int ckpt_wait(ckpt_ctx *c, uint64_t id) {
         make_sticky(c, rc);
         return rc;
     }
+    clean_pad(c, c->ongoing);
     c->completed = c->ongoing;
     c->completed_id = id;
     if (c->nbuf == 2) c->ongoing ^= 1;
@@ -1262,9 +1455,7 @@ static int rb_commit(ckpt_ctx *c, uint32_t kl, uint64_t version) {
         return rc;
     }
     if (c->me == kl) {
-        // the image's zero pad [L, L*) is structural (Q5); a lost host image had it
-        // overwritten, and the D2H above only covers [0, L)
-        if (c->Lstar > c->L) memset(c->hdata[c->ongoing].p + c->L, 0, c->Lstar - c->L);
+        clean_pad(c, c->ongoing);
         c->completed = c->ongoing;
         c->completed_id = version;
         if (c->nbuf == 2) c->ongoing ^= 1;
@@ -1356,6 +1547,7 @@ extern "C" int ckpt_forget(ckpt_ctx *c, uint8_t poison) {
     for (int i = 0; i < 2; ++i) {
         if (c->hdata[i].p) memset(c->hdata[i].p, poison, c->Lstar);
         if (c->hpar[i].p && c->m >= 2) memset(c->hpar[i].p, poison, c->Lstar / (c->m - 1));
+        c->pad_dirty[i] = c->hdata[i].p != nullptr;
     }
     c->completed = -1;
     c->completed_id = 0;

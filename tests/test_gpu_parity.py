@@ -44,7 +44,8 @@ def tiny(rank, n=9, misalign=0, device="cuda:0"):
 # ------------------------------------------------------------------ m = 1 ---------
 @pytest.mark.parametrize("n_slots,bucket,flags", [
     (0, 0, 0), (2, 4096, 0), (4, 65536, 0), (3, 1 << 20, 0),
-    (0, 0, 0x2), (2, 65536, 0x2), (4, 4096, 0x2)])
+    (0, 0, 0x2), (2, 65536, 0x2), (4, 4096, 0x2),
+    (0, 0, 0x8), (2, 65536, 0x8), (3, 4096, 0x8)])
 @pytest.mark.parametrize("misalign", [0, 1])
 def test_snapshot_unprotected_matches_oracle(torch, C, n_slots, bucket, flags, misalign):
     st = tiny(0, n=11, misalign=misalign)
@@ -132,10 +133,11 @@ def expected_group(states, Lstar, unit):
 @pytest.mark.parametrize("m", [2, 3, 4, 8])
 @pytest.mark.parametrize("unit,n_slots,bucket", [(65536, 0, 1 << 20), (4096, 3, 1 << 20), (16, 2, 4096),
                                                  (0, 0, 1 << 20), (65536, 4, 1 << 20)])
-def test_group_encode_matches_oracle(torch, C, m, unit, n_slots, bucket):
+@pytest.mark.parametrize("flags", [0, 0x10, 0x18])
+def test_group_encode_matches_oracle(torch, C, m, unit, n_slots, bucket, flags):
     if unit == 65536 and n_slots and (m - 1) * unit > bucket:
         pytest.skip("stripe larger than ring slot")
-    states, ctxs = make_group(torch, C, m, unit, n_slots, bucket)
+    states, ctxs = make_group(torch, C, m, unit, n_slots, bucket, flags=flags)
     try:
         snapshot_group(C, ctxs)
         g = C.ckpt_geometry(ctxs[0])
@@ -152,7 +154,8 @@ def test_group_encode_matches_oracle(torch, C, m, unit, n_slots, bucket):
 
 
 @pytest.mark.parametrize("m,unit,n_slots,flags", [(2, 4096, 0, 0), (3, 4096, 2, 0), (4, 65536, 0, 0x2),
-                                                  (8, 1024, 3, 0), (8, 0, 0, 0), (5, 64, 2, 0x2)])
+                                                  (8, 1024, 3, 0), (8, 0, 0, 0), (5, 64, 2, 0x2),
+                                                  (4, 4096, 2, 0x18), (6, 256, 0, 0x18)])
 def test_group_drill_rebuild_every_rank(torch, C, m, unit, n_slots, flags):
     """Failure drill (Q12): rank k loses tensors and host image; rebuild + load."""
     from synth.gpu import fill_state
