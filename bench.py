@@ -43,6 +43,8 @@ def parse():
                    help="pack kernel: 128-bit LSU, TMA bulk through SMEM, or copy engines (zero SMs)")
     p.add_argument("--gather", default="kernel", choices=["kernel", "ce"],
                    help="parity: XOR kernel reads peers over NVLink, or copy engines pull units first")
+    p.add_argument("--device-only", action="store_true",
+                   help="CKPT_OPT_DEVICE_ONLY: device-side protect only (pack + parity into HBM, no D2H)")
     p.add_argument("--no-corun", action="store_true", help="skip the co-running GEMM measurement")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu-baseline", action="store_true")
@@ -211,7 +213,10 @@ def main():
     trace("state ready")
     S = sum(s.nbytes for s in specs)
     flags = (C.CKPT_OPT_TIMING | (C.CKPT_OPT_TMA_PACK if a.pack == "tma" else 0)
-             | (C.CKPT_OPT_CE_PACK if a.pack == "ce" else 0) | (C.CKPT_OPT_CE_GATHER if a.gather == "ce" else 0))
+             | (C.CKPT_OPT_CE_PACK if a.pack == "ce" else 0) | (C.CKPT_OPT_CE_GATHER if a.gather == "ce" else 0)
+             | (C.CKPT_OPT_DEVICE_ONLY if a.device_only else 0))
+    if a.device_only:
+        a.n_slots = 0
     opts = C.ckpt_options_default(n_slots=a.n_slots, bucket_bytes=a.bucket, stripe_unit=a.unit, flags=flags)
     ctx = C.ckpt_create(local, opts)
     t_setup = time.perf_counter()
@@ -313,7 +318,7 @@ def main():
     # e2e through the public API: load (H2D of the completed image into the tensors)
     # + snapshot + commit (D2H), host wall clock, max over ranks
     e2e = None
-    if not a.no_e2e:
+    if not a.no_e2e and not a.device_only:
         C.ckpt_stats_reset(ctx)
         barrier()
         torch.cuda.synchronize()
@@ -343,12 +348,12 @@ def main():
             "scaling": "weak", "vs_baseline": None, "dtype": "u8", "data": "synthetic",
             "config": {"workload": a.config, "state_bytes_per_gpu": S, "tensors_per_gpu": len(specs),
                        "m": m, "L_star": g["L_star"], "stripe_unit": g["unit"], "bucket_bytes": a.bucket,
-                       "n_slots": a.n_slots, "pack": a.pack, "gather": a.gather,
+                       "n_slots": a.n_slots, "pack": a.pack, "gather": a.gather, "device_only": a.device_only,
                        "l2": f"inputs {S / 1e9:.2f} GB/GPU >> 126 MB L2; no flush needed"},
             "per_gpu_gbs": round(value / N, 3),
-            "host_link": {"achieved_wire_gbs_rank0": round(wire, 3), "peak_d2h_gbs_rank0_measured": round(d2h_peak, 3),
-                          "frac": round(wire / d2h_peak, 4),
-                          "note": "binding roofline of the whole step: pinned D2H of data + parity"},
+            "host_link": None if a.device_only else {
+                "achieved_wire_gbs_rank0": round(wire, 3), "peak_d2h_gbs_rank0_measured": round(d2h_peak, 3),
+                "frac": round(wire / d2h_peak, 4), "note": "binding roofline of the whole step: pinned D2H of data + parity"},
             "roofline": roof, "other_kernels": others,
             "gpu_launches": launches,
             "clocks": clocks,

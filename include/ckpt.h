@@ -67,6 +67,11 @@ extern "C" {
 #define CKPT_OPT_CE_GATHER   0x10u /* parity: copy engines pull the m-1 peer units over
                                       NVLink (2-D copies) into local HBM, then the XOR
                                       kernel runs locally at HBM speed (few SM-seconds)  */
+#define CKPT_OPT_DEVICE_ONLY 0x20u /* keep the image in HBM only: snapshot = pack + parity
+                                      into the full device staging (n_slots must be 0), no
+                                      D2H, no host arena; load/rebuild work from HBM.  A
+                                      single device image: a failed snapshot destroys the
+                                      previous one.  Measures the device-side protect path. */
 
 typedef struct ckpt_options {
     uint32_t struct_size;   /* sizeof(ckpt_options); set by ckpt_options_default       */

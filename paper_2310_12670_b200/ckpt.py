@@ -34,6 +34,7 @@ CKPT_OPT_TMA_PACK = 0x2
 CKPT_OPT_LSU_PACK = 0x4
 CKPT_OPT_CE_PACK = 0x8
 CKPT_OPT_CE_GATHER = 0x10
+CKPT_OPT_DEVICE_ONLY = 0x20
 
 CKPT_DTYPE_BYTES, CKPT_DTYPE_BF16, CKPT_DTYPE_FP16, CKPT_DTYPE_FP32 = 0, 1, 2, 3
 CKPT_ROLE_PARAM, CKPT_ROLE_MASTER, CKPT_ROLE_EXP_AVG, CKPT_ROLE_EXP_AVG_SQ, CKPT_ROLE_OTHER = 0, 1, 2, 3, 4

@@ -19,7 +19,6 @@ namespace {
 constexpr int kPackThreads = 512;
 constexpr int kPackUnroll = 4;
 constexpr int kXorThreads = 256;
-constexpr int kXorUnroll = 2;
 
 __device__ __forceinline__ uint4 ld_stream(const void *p) {
     uint4 r;
@@ -360,54 +359,60 @@ __global__ void __launch_bounds__(kTmaThreads) pack_tma_kernel(const PackArgs a)
 }
 
 // ---------------------------------------------------------------------------------
-// XOR gather.  Work is split into tiles of kXorThreads * kXorUnroll 16-byte words
+// XOR gather.  Work is split into tiles of kXorThreads * U 16-byte words
 // inside one unit, so the stripe index needs one 32-bit division per tile.
-template <int NIN>
+// NIN input streams, U words per thread per tile: NIN * U independent 128-bit loads in
+// flight per thread (8..14), enough to cover NVLink latency (~2 us) for any m.
+template <int NIN, int U>
 __global__ void __launch_bounds__(kXorThreads) xor_kernel(const XorArgs a) {
     const uint32_t words_per_unit = (uint32_t)(a.unit >> 4);
-    constexpr uint32_t kTile = kXorThreads * kXorUnroll;
-    const uint32_t tiles_per_unit = (words_per_unit + kTile - 1) / kTile;
+    constexpr uint32_t kTileW = kXorThreads * U;
+    const uint32_t tiles_per_unit = (words_per_unit + kTileW - 1) / kTileW;
     const uint64_t ntiles = a.nstripes * tiles_per_unit;
     for (uint64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
         const uint64_t s = t / tiles_per_unit;
-        const uint32_t w0 = (uint32_t)(t - s * tiles_per_unit) * kTile + threadIdx.x;
-        uint4 acc[kXorUnroll];
-        uint4 v[NIN][kXorUnroll];
+        const uint32_t w0 = (uint32_t)(t - s * tiles_per_unit) * kTileW + threadIdx.x;
+        uint4 v[NIN][U];
 #pragma unroll
         for (int k = 0; k < NIN; ++k) {
             const uint64_t base = s * a.in[k].stride + a.in[k].off;
 #pragma unroll
-            for (int u = 0; u < kXorUnroll; ++u) {
+            for (int u = 0; u < U; ++u) {
                 const uint32_t w = w0 + u * kXorThreads;
                 const uint64_t pos = base + ((uint64_t)w << 4);
                 v[k][u] = (w < words_per_unit && pos < a.in[k].valid) ? ld_cg(a.in[k].base + pos)
                                                                        : make_uint4(0, 0, 0, 0);
             }
         }
-#pragma unroll
-        for (int u = 0; u < kXorUnroll; ++u) {
-            acc[u] = v[0][u];
-#pragma unroll
-            for (int k = 1; k < NIN; ++k) {
-                acc[u].x ^= v[k][u].x;
-                acc[u].y ^= v[k][u].y;
-                acc[u].z ^= v[k][u].z;
-                acc[u].w ^= v[k][u].w;
-            }
-        }
         const uint64_t obase = s * a.out_stride + a.out_off;
 #pragma unroll
-        for (int u = 0; u < kXorUnroll; ++u) {
+        for (int u = 0; u < U; ++u) {
+            uint4 acc = v[0][u];
+#pragma unroll
+            for (int k = 1; k < NIN; ++k) {
+                acc.x ^= v[k][u].x;
+                acc.y ^= v[k][u].y;
+                acc.z ^= v[k][u].z;
+                acc.w ^= v[k][u].w;
+            }
             const uint32_t w = w0 + u * kXorThreads;
             const uint64_t pos = obase + ((uint64_t)w << 4);
-            if (w < words_per_unit && pos < a.out_valid) *reinterpret_cast<uint4 *>(a.out + pos) = acc[u];
+            if (w < words_per_unit && pos < a.out_valid) *reinterpret_cast<uint4 *>(a.out + pos) = acc;
         }
     }
 }
 
 template <int N>
-cudaError_t launch_xor_n(const XorArgs &a, int grid, cudaStream_t s) {
-    xor_kernel<N><<<grid, kXorThreads, 0, s>>>(a);
+constexpr int xor_unroll() { return N == 1 ? 8 : N == 2 ? 4 : N == 3 ? 3 : 2; }
+
+template <int N>
+cudaError_t launch_xor_n(const XorArgs &a, int max_ctas, cudaStream_t s) {
+    constexpr int U = xor_unroll<N>();
+    const uint64_t wpu = a.unit >> 4;
+    const uint64_t tpu = (wpu + kXorThreads * U - 1) / (kXorThreads * U);
+    const uint64_t ntiles = a.nstripes * tpu;
+    const int grid = (int)(ntiles < (uint64_t)max_ctas ? ntiles : (uint64_t)max_ctas);
+    xor_kernel<N, U><<<grid, kXorThreads, 0, s>>>(a);
     return cudaGetLastError();
 }
 
@@ -447,19 +452,15 @@ cudaError_t launch_pack(const PackArgs &a, int max_ctas, cudaStream_t s, bool tm
 
 cudaError_t launch_xor(const XorArgs &a, int max_ctas, cudaStream_t s) {
     if (a.nstripes == 0 || a.nin < 1 || a.nin > kMaxTerms || (a.unit & 15)) return cudaErrorInvalidValue;
-    const uint64_t wpu = a.unit >> 4;
-    const uint64_t tpu = (wpu + kXorThreads * kXorUnroll - 1) / (kXorThreads * kXorUnroll);
-    uint64_t ntiles = a.nstripes * tpu;
-    int grid = (int)(ntiles < (uint64_t)max_ctas ? ntiles : (uint64_t)max_ctas);
     switch (a.nin) {
-        case 1: return launch_xor_n<1>(a, grid, s);
-        case 2: return launch_xor_n<2>(a, grid, s);
-        case 3: return launch_xor_n<3>(a, grid, s);
-        case 4: return launch_xor_n<4>(a, grid, s);
-        case 5: return launch_xor_n<5>(a, grid, s);
-        case 6: return launch_xor_n<6>(a, grid, s);
-        case 7: return launch_xor_n<7>(a, grid, s);
-        default: return launch_xor_n<8>(a, grid, s);
+        case 1: return launch_xor_n<1>(a, max_ctas, s);
+        case 2: return launch_xor_n<2>(a, max_ctas, s);
+        case 3: return launch_xor_n<3>(a, max_ctas, s);
+        case 4: return launch_xor_n<4>(a, max_ctas, s);
+        case 5: return launch_xor_n<5>(a, max_ctas, s);
+        case 6: return launch_xor_n<6>(a, max_ctas, s);
+        case 7: return launch_xor_n<7>(a, max_ctas, s);
+        default: return launch_xor_n<8>(a, max_ctas, s);
     }
 }
 

@@ -394,6 +394,8 @@ extern "C" int ckpt_create(int device, const ckpt_options *o, ckpt_ctx **out) {
     if (opt.host_buffers != 1 && opt.host_buffers != 2) return fail(CKPT_EINVAL, "create: host_buffers must be 1 or 2");
     if (opt.n_slots == 1) return fail(CKPT_EINVAL, "create: n_slots must be 0 (full copy) or >= 2");
     if (opt.bucket_bytes < 4096) return fail(CKPT_EINVAL, "create: bucket_bytes must be >= 4096");
+    if ((opt.flags & CKPT_OPT_DEVICE_ONLY) && opt.n_slots != 0)
+        return fail(CKPT_EINVAL, "create: DEVICE_ONLY needs n_slots = 0 (the whole image in HBM)");
     if ((opt.flags & CKPT_OPT_TMA_PACK) && (opt.flags & CKPT_OPT_LSU_PACK))
         return fail(CKPT_EINVAL, "create: TMA_PACK and LSU_PACK are exclusive");
     int ndev = 0;
@@ -603,7 +605,12 @@ extern "C" int ckpt_export_handle(ckpt_ctx *c, void *buf, uint64_t *len) {
     return CKPT_OK;
 }
 
+static inline bool device_only(const ckpt_ctx *c) { return (c->opt.flags & CKPT_OPT_DEVICE_ONLY) != 0; }
+
 static int alloc_arena(ckpt_ctx *c) {
+    c->completed = -1;
+    c->ongoing = 0;
+    if (device_only(c)) return CKPT_OK;  // the image lives in the device staging
     const uint64_t pbytes = c->m >= 2 ? c->Lstar / (c->m - 1) : 0;
     for (int i = 0; i < c->nbuf; ++i) {
         int rc = host_alloc(c->hdata[i], c->Lstar);
@@ -973,7 +980,7 @@ static int do_rebuild_row(ckpt_ctx *c, uint64_t k, uint32_t kl, cudaStream_t s) 
 // The image's zero pad [L, L*) is structural (Q5) and never written by a D2H (which
 // covers [0, L)); after ckpt_forget poisoned a buffer, re-zero it before it commits.
 static void clean_pad(ckpt_ctx *c, int buf) {
-    if (buf < 0 || !c->pad_dirty[buf]) return;
+    if (buf < 0 || !c->pad_dirty[buf] || !c->hdata[buf].p) return;
     if (c->Lstar > c->L) memset(c->hdata[buf].p + c->L, 0, c->Lstar - c->L);
     c->pad_dirty[buf] = false;
 }
@@ -1133,6 +1140,14 @@ static int stage_copy(ckpt_ctx *c, uint64_t k) {
     const uint64_t bb = bucket_begin(c, k), be = bucket_end(c, k);
     const uint64_t v = valid_in_bucket(c->L, bb, be);
     CUDA_TRY(cudaStreamWaitEvent(c->sC, c->ev_packed[s], 0));
+    if (device_only(c)) {  // the image stays in HBM: only order the completion events
+        CUDA_TRY(cudaEventRecord(c->ev_d2h_data[s], c->sC));
+        if (c->m >= 2) {
+            CUDA_TRY(cudaStreamWaitEvent(c->sC, c->ev_xored[s], 0));
+            CUDA_TRY(cudaEventRecord(c->ev_d2h_par[s], c->sC));
+        }
+        return CKPT_OK;
+    }
     if (v) {
         CUDA_TRY(cudaMemcpyAsync(c->hdata[c->ongoing].p + bb, slot_ptr(c, c->staging, k), v, cudaMemcpyDeviceToHost, c->sC));
         c->st.d2h_bytes += v;
@@ -1353,15 +1368,17 @@ extern "C" int ckpt_load(ckpt_ctx *c, void *stream) {
     c->seq = saved_seq;  // local op: no group sequence numbers consumed
     CUDA_TRY(cudaEventRecord(c->ev_capture, caller));
     CUDA_TRY(cudaStreamWaitEvent(c->sC, c->ev_capture, 0));
-    const uint8_t *img = c->hdata[c->completed].p;
+    const uint8_t *img = device_only(c) ? nullptr : c->hdata[c->completed].p;
     for (uint64_t k = 0; k < c->op_NB; ++k) {
         const uint32_t s = slot_of(c, k);
         const uint64_t bb = bucket_begin(c, k);
         const uint64_t v = valid_in_bucket(c->L, bb, bucket_end(c, k));
         if (!v) continue;
         if (ring_reuse(c, k)) CUDA_TRY(cudaStreamWaitEvent(c->sC, c->ev_kdone[s], 0));
-        CUDA_TRY(cudaMemcpyAsync(slot_ptr(c, c->staging, k), img + bb, v, cudaMemcpyHostToDevice, c->sC));
-        c->st.h2d_bytes += v;
+        if (!device_only(c)) {
+            CUDA_TRY(cudaMemcpyAsync(slot_ptr(c, c->staging, k), img + bb, v, cudaMemcpyHostToDevice, c->sC));
+            c->st.h2d_bytes += v;
+        }
         CUDA_TRY(cudaEventRecord(c->ev_h2d[s], c->sC));
         CUDA_TRY(cudaStreamWaitEvent(c->sP, c->ev_h2d[s], 0));
         if ((rc = do_pack(c, k, slot_ptr(c, c->staging, k), c->sP, true))) return rc;
@@ -1394,10 +1411,12 @@ static int rb_stage1(ckpt_ctx *c, uint64_t b, uint32_t kl) {
             if ((rc = wait_all(c, c->sC, kRel, bucket_seq(c, b - c->n_slots), s))) return rc;
         }
         const uint64_t v = valid_in_bucket(c->L, bb, be);
-        if (v) CUDA_TRY(cudaMemcpyAsync(slot_ptr(c, c->staging, b), c->hdata[c->completed].p + bb, v, cudaMemcpyHostToDevice, c->sC));
         const uint64_t pb = (be - bb) / (c->m - 1);
-        CUDA_TRY(cudaMemcpyAsync(parity_slot_ptr(c, b), c->hpar[c->completed].p + bb / (c->m - 1), pb, cudaMemcpyHostToDevice, c->sC));
-        c->st.h2d_bytes += v + pb;
+        if (!device_only(c)) {  // device-only: staging and parity already hold the image
+            if (v) CUDA_TRY(cudaMemcpyAsync(slot_ptr(c, c->staging, b), c->hdata[c->completed].p + bb, v, cudaMemcpyHostToDevice, c->sC));
+            CUDA_TRY(cudaMemcpyAsync(parity_slot_ptr(c, b), c->hpar[c->completed].p + bb / (c->m - 1), pb, cudaMemcpyHostToDevice, c->sC));
+            c->st.h2d_bytes += v + pb;
+        }
         CUDA_TRY(cudaEventRecord(c->ev_h2d[s], c->sC));
         return sig_signal(c, c->sC, kReady, bucket_seq(c, b), s);
     }
@@ -1430,12 +1449,15 @@ static int rb_stage3(ckpt_ctx *c, uint64_t b, uint32_t kl) {
     if ((rc = wait_all(c, c->sC, kRel, bucket_seq(c, b), s))) return rc;
     CUDA_TRY(cudaStreamWaitEvent(c->sC, c->ev_kdone[s], 0));
     const uint64_t v = valid_in_bucket(c->L, bb, be);
-    if (v) CUDA_TRY(cudaMemcpyAsync(c->hdata[c->ongoing].p + bb, slot_ptr(c, c->staging, b), v, cudaMemcpyDeviceToHost, c->sC));
-    CUDA_TRY(cudaEventRecord(c->ev_d2h_data[s], c->sC));
     const uint64_t pb = (be - bb) / (c->m - 1);
-    CUDA_TRY(cudaMemcpyAsync(c->hpar[c->ongoing].p + bb / (c->m - 1), parity_slot_ptr(c, b), pb, cudaMemcpyDeviceToHost, c->sC));
+    if (!device_only(c) && v)
+        CUDA_TRY(cudaMemcpyAsync(c->hdata[c->ongoing].p + bb, slot_ptr(c, c->staging, b), v, cudaMemcpyDeviceToHost, c->sC));
+    CUDA_TRY(cudaEventRecord(c->ev_d2h_data[s], c->sC));
+    if (!device_only(c)) {
+        CUDA_TRY(cudaMemcpyAsync(c->hpar[c->ongoing].p + bb / (c->m - 1), parity_slot_ptr(c, b), pb, cudaMemcpyDeviceToHost, c->sC));
+        c->st.d2h_bytes += v + pb;
+    }
     CUDA_TRY(cudaEventRecord(c->ev_d2h_par[s], c->sC));
-    c->st.d2h_bytes += v + pb;
     return CKPT_OK;
 }
 
@@ -1544,6 +1566,13 @@ extern "C" int ckpt_rebuild(ckpt_ctx *c, int32_t lost, void *stream) {
 extern "C" int ckpt_forget(ckpt_ctx *c, uint8_t poison) {
     if (!c) return fail(CKPT_EINVAL, "forget: null");
     if (c->pending_id || c->requested) return fail(CKPT_ESTATE, "forget: a snapshot is in flight");
+    if (device_only(c) && c->staging) {  // the image is in HBM: poison staging + parity
+        int rc = set_dev(c);
+        if (rc) return rc;
+        CUDA_TRY(cudaMemset(c->staging, poison, c->staging_bytes));
+        if (c->parity) CUDA_TRY(cudaMemset(c->parity, poison, c->parity_bytes));
+        CUDA_TRY(cudaDeviceSynchronize());
+    }
     for (int i = 0; i < 2; ++i) {
         if (c->hdata[i].p) memset(c->hdata[i].p, poison, c->Lstar);
         if (c->hpar[i].p && c->m >= 2) memset(c->hpar[i].p, poison, c->Lstar / (c->m - 1));
@@ -1558,6 +1587,7 @@ extern "C" int ckpt_host_view(const ckpt_ctx *c, int which, const void **data, u
                               uint64_t *plen) {
     if (!c || (which != 0 && which != 1)) return fail(CKPT_EINVAL, "host_view: bad args");
     if (!c->grouped) return fail(CKPT_ENOSNAP, "host_view: no host arena yet");
+    if (device_only(c)) return fail(CKPT_EINVAL, "host_view: DEVICE_ONLY context has no host image");
     int idx = which == 0 ? c->completed : c->ongoing;
     if (idx < 0) return fail(CKPT_ENOSNAP, "host_view: no completed snapshot");
     if (data) *data = c->hdata[idx].p;

@@ -301,3 +301,39 @@ def test_c2_7b_tp8_rank_sampled(torch, C):
             assert_bytes_equal(got, oracle.fill(synth.SEED, 3, int(t), n), f"tensor {t} after load")
     finally:
         C.ckpt_destroy(ctx)
+
+
+@pytest.mark.parametrize("m,unit,flags", [(1, 65536, 0x20), (3, 4096, 0x20), (4, 65536, 0x22), (8, 1024, 0x28),
+                                          (5, 256, 0x30)])
+def test_device_only_drill(torch, C, m, unit, flags):
+    """DEVICE_ONLY: the image and parity stay in HBM; every lost rank is rebuilt from
+    the survivors' device images and reloaded bit-exactly."""
+    from synth.gpu import fill_state
+    states = [tiny(j, n=6 + j % 2, misalign=1) for j in range(m)]
+    ctxs = [make_ctx(C, st, n_slots=0, bucket_bytes=1 << 16, stripe_unit=unit, flags=flags) for st in states]
+    try:
+        if m == 1:
+            assert C.ckpt_protect(ctxs[0], 1, 0) == C.CKPT_EUNAVAIL
+        else:
+            C.protect_local(ctxs)
+        snapshot_group(C, ctxs)
+        with pytest.raises(C.CkptError):
+            C.ckpt_host_view(ctxs[0], 0)
+        for k in range(m):
+            for j, (_, ts) in enumerate(states):
+                fill_state(ts, j, seed=31 + k, xor_mode=1)
+            if m > 1:
+                C.ckpt_forget(ctxs[k], 0x5A)
+                for t in states[k][1]:
+                    t.view(torch.uint8).fill_(0x5A)
+                for c in ctxs:
+                    C.ckpt_rebuild(c, k)
+            for c in ctxs:
+                C.ckpt_load(c)
+            torch.cuda.synchronize()
+            for j, (specs, ts) in enumerate(states):
+                for t, (x, w) in enumerate(zip(ts, oracle_tensor_bytes(specs, j))):
+                    assert_bytes_equal(tensor_bytes(x), w, f"k={k}: rank {j} tensor {t}")
+    finally:
+        for c in ctxs:
+            C.ckpt_destroy(c)

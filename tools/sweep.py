@@ -1,0 +1,129 @@
+#!/usr/bin/env python3
+"""Per-config measurements for SURVEY.md 8(d) (C1-C5), one process per GPU.
+
+  torchrun --nproc-per-node N tools/sweep.py --config c3_13b_tp4pp2 --buckets 4,16,64,256,512 --drill
+  python tools/sweep.py --config c2_7b_tp8            (N = 1)
+
+For every bucket size (MiB): snapshot+protect time (median of reps, max over ranks),
+state GB/s per GPU, wire GB/s, device-side protect (DEVICE_ONLY) time, and with --drill
+the rebuild of lost rank k plus the distributed in-memory load (C5), with a bit-exact
+check of the rebuilt rank's tensors against the generator.  JSON lines on rank 0."""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+
+def main():
+    p = argparse.ArgumentParser()
+    p.add_argument("--config", default="c2_7b_tp8")
+    p.add_argument("--buckets", default="64")
+    p.add_argument("--reps", type=int, default=3)
+    p.add_argument("--n-slots", type=int, default=4)
+    p.add_argument("--unit", type=int, default=65536)
+    p.add_argument("--flags", type=int, default=0)
+    p.add_argument("--drill", action="store_true")
+    p.add_argument("--device-only", action="store_true")
+    p.add_argument("--lost", default="")
+    a = p.parse_args()
+    import torch
+    import torch.distributed as dist
+
+    from paper_2310_12670_b200 import ckpt as C
+    from synth.gpu import descriptors, fill_state, make_rank_state
+
+    rank, world = int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1))
+    local = int(os.environ.get("LOCAL_RANK", 0))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+
+    def bar():
+        if world > 1:
+            dist.barrier()
+
+    def amax(x):
+        if world == 1:
+            return x
+        t = torch.tensor([float(x)], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    specs, ts = make_rank_state(a.config, rank, dev)
+    S = sum(s.nbytes for s in specs)
+    for bmib in [int(x) for x in a.buckets.split(",")]:
+        flags = a.flags | C.CKPT_OPT_TIMING | (C.CKPT_OPT_DEVICE_ONLY if a.device_only else 0)
+        n_slots = 0 if a.device_only else a.n_slots
+        ctx = C.ckpt_create(local, C.ckpt_options_default(bucket_bytes=bmib << 20, n_slots=n_slots,
+                                                          stripe_unit=a.unit, flags=flags))
+        C.ckpt_register(ctx, descriptors(ts, specs))
+        if world > 1:
+            C.protect_ipc(ctx)
+        else:
+            C.ckpt_protect(ctx, 1, 0)
+        g = C.ckpt_geometry(ctx)
+        st0 = torch.cuda.current_stream()
+        times = []
+        for r in range(a.reps + 1):
+            bar()
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            sid = C.ckpt_snapshot(ctx, 0, st0)
+            C.ckpt_wait(ctx, sid)
+            dt = amax(time.perf_counter() - t0)
+            if r:
+                times.append(dt)
+        st = C.ckpt_get_stats(ctx)
+        t = statistics.median(times)
+        rec = {"config": a.config, "m": g["m"], "bucket_mib": bmib, "n_slots": n_slots, "flags": flags,
+               "state_bytes": S, "L_star": g["L_star"], "snapshot_ms": round(t * 1e3, 3),
+               "state_gbs_per_gpu": round(S / t / 1e9, 3), "wire_gbs_per_gpu": round(st["d2h_bytes"] / (a.reps + 1) / t / 1e9, 3),
+               "pack_us_per_launch": round(st["pack_ms"] / max(st["pack_launches"], 1) * 1e3, 2),
+               "xor_us_per_launch": round(st["xor_ms"] / max(st["xor_launches"], 1) * 1e3, 2),
+               "pack_hbm_gbs": round(st["pack_bytes"] / max(st["pack_ms"], 1e-9) / 1e6, 1),
+               "xor_nvlink_gbs": round(st["xor_bytes_in"] / max(st["xor_ms"], 1e-9) / 1e6, 1),
+               "launches_per_snapshot": (st["pack_launches"] + st["xor_launches"]) // (a.reps + 1)}
+        if a.drill and g["m"] >= 2:
+            lost = [int(x) for x in a.lost.split(",")] if a.lost else [0, g["m"] - 1]
+            for k in lost:
+                fill_state(ts, rank, seed=999 + k, xor_mode=1)  # later steps mutate everything
+                if rank == k:
+                    C.ckpt_forget(ctx, 0xA5)
+                    for x in ts:
+                        x.view(torch.uint8).fill_(0xA5)
+                bar()
+                torch.cuda.synchronize()
+                t0 = time.perf_counter()
+                C.ckpt_rebuild(ctx, k)
+                t1 = time.perf_counter()
+                C.ckpt_load(ctx)
+                torch.cuda.synchronize()
+                t2 = time.perf_counter()
+                rb, ld = amax(t1 - t0), amax(t2 - t1)
+                # bit-exact: every tensor of every rank equals the generator (sampled bytes)
+                ok = True
+                from synth import SEED, fill as gfill
+                for ti in range(0, len(ts), max(1, len(ts) // 16)):
+                    n = min(specs[ti].nbytes, 1 << 16)
+                    got = ts[ti].view(torch.uint8)[:n].cpu().numpy()
+                    ok = ok and bool((got == gfill(SEED, rank, ti, n)).all())
+                okall = amax(0.0 if ok else 1.0) == 0.0
+                rec.setdefault("drill", []).append({"lost": k, "rebuild_ms": round(rb * 1e3, 2), "load_ms": round(ld * 1e3, 2),
+                                                    "bit_exact_sampled": okall})
+        if rank == 0:
+            print(json.dumps(rec), flush=True)
+        C.ckpt_destroy(ctx)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

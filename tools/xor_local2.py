@@ -1,0 +1,63 @@
+#!/usr/bin/env python3
+"""One process, m GPUs: a CKPT_GROUP_LOCAL group whose members sit on different devices,
+so the XOR encode reads its peers over NVLink inside a single process -- the only way to
+put the NVLink-bound kernel under ncu (never a multi-rank command).
+
+  python tools/xor_local2.py [--m 2] [--config c2_7b_tp8] [--reps 3] [--device-only]
+
+Prints per-kernel mean launch times and NVLink GB/s (CUDA events on the launch stream)."""
+import argparse
+import json
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+
+def main():
+    p = argparse.ArgumentParser()
+    p.add_argument("--m", type=int, default=2)
+    p.add_argument("--config", default="c2_7b_tp8")
+    p.add_argument("--reps", type=int, default=3)
+    p.add_argument("--bucket", type=int, default=64 << 20)
+    p.add_argument("--flags", type=int, default=0)
+    a = p.parse_args()
+    import torch
+
+    from paper_2310_12670_b200 import ckpt as C
+    from synth.gpu import descriptors, make_rank_state
+
+    m = min(a.m, torch.cuda.device_count())
+    ctxs, states = [], []
+    for j in range(m):
+        torch.cuda.set_device(j)
+        specs, ts = make_rank_state(a.config, j, torch.device("cuda", j))
+        c = C.ckpt_create(j, C.ckpt_options_default(n_slots=0, bucket_bytes=a.bucket,
+                                                    flags=C.CKPT_OPT_TIMING | C.CKPT_OPT_DEVICE_ONLY | a.flags))
+        C.ckpt_register(c, descriptors(ts, specs))
+        ctxs.append(c)
+        states.append((specs, ts))
+    C.protect_local(ctxs)
+    for r in range(a.reps + 1):
+        if r == 1:
+            for c in ctxs:
+                C.ckpt_stats_reset(c)
+        ids = []
+        for j, c in enumerate(ctxs):
+            torch.cuda.set_device(j)
+            ids.append(C.ckpt_snapshot(c, 0, torch.cuda.current_stream(j)))
+        for c, i in zip(ctxs, ids):
+            C.ckpt_wait(c, i)
+    st = C.ckpt_get_stats(ctxs[0])
+    print(json.dumps({"m": m, "config": a.config, "pack_us": st["pack_ms"] / max(st["pack_launches"], 1) * 1e3,
+                      "xor_us": st["xor_ms"] / max(st["xor_launches"], 1) * 1e3,
+                      "xor_nvlink_gbs": st["xor_bytes_in"] / max(st["xor_ms"], 1e-9) / 1e6,
+                      "pack_hbm_gbs": st["pack_bytes"] / max(st["pack_ms"], 1e-9) / 1e6,
+                      "snapshot_ms": st["last_snapshot_ms"]}))
+    for c in ctxs:
+        C.ckpt_destroy(c)
+
+
+if __name__ == "__main__":
+    main()
