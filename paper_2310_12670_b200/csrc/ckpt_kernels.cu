@@ -160,15 +160,15 @@ __device__ __forceinline__ uint64_t clip_chunk(const PackArgs &a, const PackChun
 // odd-sized tails, small gaps) take the block-cooperative funnel-shift path.
 constexpr int kBatch = 128;
 
-__global__ void __launch_bounds__(kPackThreads) pack_kernel(const PackArgs a) {
+// Flat copy of the chunks [cb, ce) (clipped to a's bucket): descriptors staged in
+// SMEM by batches of kBatch, the 16-B-aligned chunks streamed as one flat word space.
+__device__ __forceinline__ void copy_chunks(const PackArgs &a, uint64_t cb, uint64_t ce) {
     __shared__ const uint8_t *s_from[kBatch];
     __shared__ uint8_t *s_to[kBatch];
     __shared__ uint64_t s_n[kBatch];
     __shared__ uint32_t s_pre[kBatch + 1];
     __shared__ uint32_t s_nslow;
     __shared__ uint8_t s_slow[kBatch];
-    uint64_t cb, ce;
-    cta_chunk_range(a, cb, ce);
     const uint32_t tid = threadIdx.x, nt = blockDim.x;
     for (uint64_t c0 = cb; c0 < ce; c0 += kBatch) {
         const uint32_t nb = (uint32_t)((ce - c0) < kBatch ? (ce - c0) : kBatch);
@@ -220,6 +220,48 @@ __global__ void __launch_bounds__(kPackThreads) pack_kernel(const PackArgs a) {
                 block_zero(s_to[j], s_n[j]);
         }
         __syncthreads();
+    }
+}
+
+__global__ void __launch_bounds__(kPackThreads) pack_kernel(const PackArgs a) {
+    uint64_t cb, ce;
+    cta_chunk_range(a, cb, ce);
+    copy_chunks(a, cb, ce);
+}
+
+__device__ __forceinline__ void st_release_sys(uint32_t *p, uint32_t v) {
+    asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+__global__ void __launch_bounds__(kPackThreads) pack_all_kernel(const PackAllArgs g) {
+    PackArgs a;
+    a.chunks = g.chunks;
+    a.tile_first = g.tile_first;
+    a.bucket_begin = 0;
+    a.bucket_end = g.L;
+    a.slot = g.image;
+    a.unpack = 0;
+    const uint64_t ntiles = (g.L + kTile - 1) / kTile;
+    const uint64_t ngroups = (g.L + kGroup - 1) / kGroup;
+    const uint64_t tiles_per_group = kGroup / kTile;
+    for (uint64_t grp = blockIdx.x; grp < ngroups; grp += gridDim.x) {
+        const uint64_t t0 = grp * tiles_per_group;
+        const uint64_t t1 = t0 + tiles_per_group < ntiles ? t0 + tiles_per_group : ntiles;
+        copy_chunks(a, g.tile_first[t0], g.tile_first[t1]);  // ends with __syncthreads()
+        if (threadIdx.x == 0) {
+            __threadfence();  // the CTA's stores (ordered by the barrier) before the count
+            const uint64_t k = grp * kGroup / g.bucket;
+            const uint64_t lo = k * g.bucket;
+            const uint64_t hi = lo + g.bucket < g.L ? lo + g.bucket : g.L;
+            const uint32_t need = (uint32_t)((hi - lo + kGroup - 1) / kGroup);
+            if (atomicAdd(&g.counters[k], 1u) + 1 == need) {
+                __threadfence_system();
+                const uint32_t v = g.seq_base + (uint32_t)k + 1;
+                const uint32_t i = v % g.maxb;
+                st_release_sys(g.ready_local + i, v);
+                for (int p = 0; p < g.npeers; ++p) st_release_sys(g.ready_peer[p] + i, v);
+            }
+        }
     }
 }
 
@@ -422,6 +464,14 @@ __global__ void signal_kernel(const SignalArgs a) {
 }
 
 }  // namespace
+
+cudaError_t launch_pack_all(const PackAllArgs &a, int max_ctas, cudaStream_t s) {
+    const uint64_t ngroups = (a.L + kGroup - 1) / kGroup;
+    if (ngroups == 0) return cudaSuccess;
+    const uint64_t g = ngroups < (uint64_t)max_ctas ? ngroups : (uint64_t)max_ctas;
+    pack_all_kernel<<<(unsigned)g, kPackThreads, 0, s>>>(a);
+    return cudaGetLastError();
+}
 
 cudaError_t launch_signal(const SignalArgs &a, cudaStream_t s) {
     signal_kernel<<<1, 32, 0, s>>>(a);

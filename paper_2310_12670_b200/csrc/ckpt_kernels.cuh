@@ -6,6 +6,8 @@
 
 namespace reft {
 
+constexpr int kMaxTerms = 8;
+
 // One contiguous piece of the packed image: bytes [dst, dst + nbytes) of the image
 // come from device address src (src == 0: zero fill -- alignment gaps, reading Q6).
 // Built once by the planner at ckpt_register; sorted by dst.
@@ -42,7 +44,6 @@ struct XorTerm {
     uint64_t off;
 };
 
-constexpr int kMaxTerms = 8;
 
 // out[s * out_stride + out_off + w] = XOR_t in_t[s * stride_t + off_t + w] for every
 // stripe s < nstripes and byte w < unit (unit a multiple of 16).  Writes at or
@@ -60,6 +61,28 @@ struct XorArgs {
     uint64_t unit;
 };
 
+// Whole-snapshot pack in ONE launch (full-copy staging): CTAs stride over 64 KiB
+// groups of image tiles in order; the last CTA to finish a bucket publishes it: a
+// release store of flag value seq_base+k+1 at index (value % maxb) of this rank's READY
+// row, locally (the copy engine's D2H of bucket k waits on it with cuStreamWaitValue32)
+// and in every peer's IPC-mapped flag page (their XOR of bucket k waits on it).  No
+// kernel ever waits on another; only stream memory operations wait.
+constexpr uint64_t kGroup = 4 * kTile;
+
+struct PackAllArgs {
+    const PackChunk *chunks;
+    const uint32_t *tile_first;
+    uint64_t L;            // image bytes to pack: [0, L)
+    uint8_t *image;        // staging address of image byte 0
+    uint64_t bucket;       // B, a multiple of kGroup
+    uint32_t *counters;    // per bucket, zeroed before the launch
+    uint32_t *ready_local; // this rank's READY row in its own flag page
+    uint32_t *ready_peer[kMaxTerms];  // this rank's READY row in each peer's page
+    int npeers;
+    uint32_t seq_base;
+    uint32_t maxb;
+};
+
 // Cross-rank signal by a one-warp kernel: st.release.sys of `value` to every address
 // (peers' IPC-mapped flag words).  Alternative to cuStreamWriteValue32 (CKPT_SIGNAL=kernel).
 struct SignalArgs {
@@ -70,6 +93,7 @@ struct SignalArgs {
 
 // Launchers (return the cudaError_t of the launch).
 cudaError_t launch_signal(const SignalArgs &a, cudaStream_t s);
+cudaError_t launch_pack_all(const PackAllArgs &a, int max_ctas, cudaStream_t s);
 cudaError_t launch_pack(const PackArgs &a, int max_ctas, cudaStream_t s, bool tma);
 cudaError_t launch_xor(const XorArgs &a, int max_ctas, cudaStream_t s);
 

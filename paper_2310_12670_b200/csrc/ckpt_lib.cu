@@ -24,6 +24,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <mutex>
+#include <numeric>
 #include <string>
 #include <thread>
 #include <vector>
@@ -86,7 +87,12 @@ constexpr uint32_t kAbiVersion = 1;
 // flag page: 3 arrays of CKPT_MAX_GROUP uint32, each on its own 128-B line
 enum Stage { kReady = 0, kRel = 1, kDone = 2, kNumStages = 3 };
 constexpr uint64_t kFlagStride = 32;  // uint32 per stage line
-constexpr uint64_t kFlagBytes = 4096;
+constexpr uint64_t kFlagBytes = 4096;  // REL and DONE lines (READY line unused)
+// READY is per bucket: row j (written by member j) holds the flag of bucket seq at index
+// seq % kMaxB -- per-bucket because the single-launch pack completes buckets out of order.
+constexpr uint32_t kMaxB = 16384;
+constexpr uint64_t kFlagAlloc = kFlagBytes + (uint64_t)CKPT_MAX_GROUP * kMaxB * 4;
+inline uint32_t *ready_row(uint32_t *flags, uint32_t j) { return flags + kFlagBytes / 4 + (uint64_t)j * kMaxB; }
 
 struct HandleBlob {  // exported by ckpt_export_handle; fixed layout, <= CKPT_HANDLE_BYTES
     uint32_t magic, version;
@@ -150,6 +156,7 @@ struct ckpt_ctx {
     uint8_t *staging = nullptr;
     uint64_t staging_bytes = 0;
     uint32_t *flags = nullptr;  // local flag page (device), written by peers
+    uint32_t *counters = nullptr;  // per-bucket CTA completion counters (single-launch pack)
 
     // group
     bool grouped = false;  // ckpt_protect succeeded (m >= 2) or m == 1 arena set up
@@ -468,6 +475,7 @@ extern "C" int ckpt_destroy(ckpt_ctx *c) {
     if (c->d_chunks) cudaFree(c->d_chunks);
     if (c->staging) cudaFree(c->staging);
     if (c->flags) cudaFree(c->flags);
+    if (c->counters) cudaFree(c->counters);
     if (c->parity) cudaFree(c->parity);
     if (c->gather) cudaFree(c->gather);
     for (int i = 0; i < 2; ++i) {
@@ -541,14 +549,18 @@ extern "C" int ckpt_register(ckpt_ctx *c, const ckpt_tensor *t, uint64_t n, cons
     CUDA_TRY(cudaMemcpy((uint8_t *)dch + tbytes, tf.data(), fbytes, cudaMemcpyHostToDevice));
     c->d_tile_first = (const uint32_t *)((uint8_t *)dch + tbytes);
     if (cudaMalloc(&c->staging, c->staging_bytes) != cudaSuccess ||
-        cudaMalloc(&c->flags, kFlagBytes) != cudaSuccess) {
+        cudaMalloc(&c->flags, kFlagAlloc) != cudaSuccess) {
         cudaGetLastError();
         cudaFree(dch);
         if (c->staging) cudaFree(c->staging);
         c->staging = nullptr;
         return fail(CKPT_ENOMEM, "register: device staging of %llu bytes failed", (unsigned long long)c->staging_bytes);
     }
-    CUDA_TRY(cudaMemset(c->flags, 0, kFlagBytes));
+    CUDA_TRY(cudaMemset(c->flags, 0, kFlagAlloc));
+    if (cudaMalloc(&c->counters, kMaxB * sizeof(uint32_t)) != cudaSuccess) {
+        cudaGetLastError();
+        return fail(CKPT_ENOMEM, "register: bucket counters allocation failed");
+    }
     CUDA_TRY(cudaMemset(c->staging, 0, c->staging_bytes));
     c->d_chunks = dch;
     c->tile_first = std::move(tf);
@@ -800,18 +812,22 @@ static bool signal_by_kernel() {
 static int sig_signal(ckpt_ctx *c, cudaStream_t s, int stage, uint32_t seq, uint32_t slot) {
     if (c->m < 2) return CKPT_OK;
     if (c->transport == CKPT_GROUP_IPC) {
+        auto addr = [&](uint32_t j) {
+            return stage == kReady ? ready_row(c->peer_flags[j], c->me) + seq % kMaxB
+                                   : c->peer_flags[j] + stage * kFlagStride + c->me;
+        };
         if (signal_by_kernel()) {
             SignalArgs a;
             memset(&a, 0, sizeof a);
             for (uint32_t j = 0; j < c->m; ++j)
-                if (j != c->me) a.addr[a.n++] = c->peer_flags[j] + stage * kFlagStride + c->me;
+                if (j != c->me) a.addr[a.n++] = addr(j);
             a.value = seq;
             CUDA_TRY(launch_signal(a, s));
             return CKPT_OK;
         }
         for (uint32_t j = 0; j < c->m; ++j) {
             if (j == c->me) continue;
-            CUdeviceptr a = (CUdeviceptr)(uintptr_t)(c->peer_flags[j] + stage * kFlagStride + c->me);
+            CUdeviceptr a = (CUdeviceptr)(uintptr_t)addr(j);
             CUresult r = p_write32((CUstream)s, a, seq, CU_STREAM_WRITE_VALUE_DEFAULT);
             if (r != CUDA_SUCCESS) return fail(CKPT_ECUDA, "cuStreamWriteValue32 failed (%d)", (int)r);
         }
@@ -826,7 +842,8 @@ static int sig_signal(ckpt_ctx *c, cudaStream_t s, int stage, uint32_t seq, uint
 // wait(stage, seq): stream s waits until member j signalled >= seq.
 static int sig_wait(ckpt_ctx *c, cudaStream_t s, uint32_t j, int stage, uint32_t seq, uint32_t slot) {
     if (c->transport == CKPT_GROUP_IPC) {
-        CUdeviceptr a = (CUdeviceptr)(uintptr_t)(c->flags + stage * kFlagStride + j);
+        CUdeviceptr a = (CUdeviceptr)(uintptr_t)(stage == kReady ? ready_row(c->flags, j) + seq % kMaxB
+                                                                   : c->flags + stage * kFlagStride + j);
         CUresult r = p_wait32((CUstream)s, a, seq, CU_STREAM_WAIT_VALUE_GEQ);
         if (r != CUDA_SUCCESS) return fail(CKPT_ECUDA, "cuStreamWaitValue32 failed (%d)", (int)r);
         return CKPT_OK;
@@ -997,20 +1014,66 @@ static void make_sticky(ckpt_ctx *c, int rc) {
     }
 }
 
+// Bucket = whole stripes ((m-1)u; A when unprotected).  With full-copy staging the
+// single-launch pack also needs whole 64 KiB tile groups: B is rounded down to a
+// multiple of lcm(stripe, kGroup).
 static uint64_t effective_bucket(const ckpt_ctx *c, uint64_t req) {
     uint64_t B = req ? req : c->opt.bucket_bytes;
-    if (c->m >= 2) {
-        const uint64_t stripe = (uint64_t)(c->m - 1) * c->unit;
-        B = std::max<uint64_t>(stripe, B / stripe * stripe);
-    } else {
-        B = std::max<uint64_t>(c->opt.align, B / c->opt.align * c->opt.align);
+    uint64_t q = c->m >= 2 ? (uint64_t)(c->m - 1) * c->unit : (uint64_t)c->opt.align;
+    if (c->full_copy) q = q / std::gcd(q, kGroup) * kGroup;
+    return std::max<uint64_t>(q, B / q * q);
+}
+
+static bool single_launch(const ckpt_ctx *c) {
+    return c->full_copy && !(c->opt.flags & (CKPT_OPT_CE_PACK | CKPT_OPT_TMA_PACK)) &&
+           (c->transport == CKPT_GROUP_LOCAL && c->m >= 2 ? true : load_memops() == CKPT_OK);
+}
+
+// The whole snapshot's pack as one launch (full-copy staging); the kernel publishes each
+// bucket's READY flag itself (see PackAllArgs).  Buckets past this rank's L hold no data
+// and are published up front.
+static int issue_pack_all(ckpt_ctx *c) {
+    const uint64_t nb_data = (c->L + c->op_B - 1) / c->op_B;
+    int rc;
+    CUDA_TRY(cudaMemsetAsync(c->counters, 0, std::max<uint64_t>(nb_data, 1) * sizeof(uint32_t), c->sP));
+    if (c->m >= 2)
+        for (uint64_t k = nb_data; k < c->op_NB; ++k)
+            if ((rc = sig_signal(c, c->sP, kReady, bucket_seq(c, k), slot_of(c, k)))) return rc;
+    PackAllArgs a;
+    memset(&a, 0, sizeof a);
+    a.chunks = c->d_chunks;
+    a.tile_first = c->d_tile_first;
+    a.L = c->L;
+    a.image = c->staging;
+    a.bucket = c->op_B;
+    a.counters = c->counters;
+    a.ready_local = ready_row(c->flags, c->me);
+    if (c->m >= 2 && c->transport == CKPT_GROUP_IPC)
+        for (uint32_t j = 0; j < c->m; ++j)
+            if (j != c->me) a.ready_peer[a.npeers++] = ready_row(c->peer_flags[j], c->me);
+    a.seq_base = c->op_seq_base;
+    a.maxb = kMaxB;
+    TimedLaunch *t;
+    if ((rc = timed_begin(c, c->sP, 0, &t))) return rc;
+    CUDA_TRY(launch_pack_all(a, c->max_ctas, c->sP));
+    if ((rc = timed_end(t, c->sP))) return rc;
+    c->st.pack_launches++;
+    c->st.pack_bytes += 2 * c->L;
+    if (c->transport == CKPT_GROUP_LOCAL && c->m >= 2) {
+        for (uint64_t k = 0; k < nb_data; ++k) {
+            CUDA_TRY(cudaEventRecord(c->ev_packed[slot_of(c, k)], c->sP));
+            if ((rc = sig_signal(c, c->sP, kReady, bucket_seq(c, k), slot_of(c, k)))) return rc;
+        }
     }
-    return B;
+    return CKPT_OK;
 }
 
 static int prepare_op(ckpt_ctx *c, uint64_t B) {
+    const uint64_t nb = c->Lstar ? (c->Lstar + B - 1) / B : 0;
+    if (nb >= kMaxB) return fail(CKPT_EINVAL, "bucket of %llu bytes gives %llu buckets (max %u): use larger buckets",
+                                 (unsigned long long)B, (unsigned long long)nb, kMaxB - 1);
     c->op_B = B;
-    c->op_NB = c->Lstar ? (c->Lstar + B - 1) / B : 0;
+    c->op_NB = nb;
     c->op_seq_base = c->seq;
     c->seq += (uint32_t)c->op_NB + 1;
     const size_t ne = c->full_copy ? (size_t)std::max<uint64_t>(c->op_NB, 1) : c->n_slots;
@@ -1126,7 +1189,7 @@ static int stage_xor(ckpt_ctx *c, uint64_t k) {
         CUDA_TRY(cudaEventRecord(c->ev_xored[s], c->sX));
         return CKPT_OK;
     }
-    CUDA_TRY(cudaStreamWaitEvent(c->sX, c->ev_packed[s], 0));
+    // row me reads only the peers' units: no wait on this rank's own pack
     if ((rc = wait_all(c, c->sX, kReady, bucket_seq(c, k), s))) return rc;
     if (ring_reuse(c, k)) CUDA_TRY(cudaStreamWaitEvent(c->sX, c->ev_d2h_par[s], 0));
     if ((rc = do_encode(c, k, c->sX))) return rc;
@@ -1139,7 +1202,16 @@ static int stage_copy(ckpt_ctx *c, uint64_t k) {
     const uint32_t s = slot_of(c, k);
     const uint64_t bb = bucket_begin(c, k), be = bucket_end(c, k);
     const uint64_t v = valid_in_bucket(c->L, bb, be);
-    CUDA_TRY(cudaStreamWaitEvent(c->sC, c->ev_packed[s], 0));
+    if (single_launch(c) && !(c->transport == CKPT_GROUP_LOCAL && c->m >= 2)) {
+        if (v) {  // the single pack kernel publishes bucket k in this rank's READY row
+            const uint32_t q = bucket_seq(c, k);
+            CUresult r = p_wait32((CUstream)c->sC, (CUdeviceptr)(uintptr_t)(ready_row(c->flags, c->me) + q % kMaxB), q,
+                                  CU_STREAM_WAIT_VALUE_GEQ);
+            if (r != CUDA_SUCCESS) return fail(CKPT_ECUDA, "cuStreamWaitValue32 failed (%d)", (int)r);
+        }
+    } else if (v || !single_launch(c)) {
+        CUDA_TRY(cudaStreamWaitEvent(c->sC, c->ev_packed[s], 0));
+    }
     if (device_only(c)) {  // the image stays in HBM: only order the completion events
         CUDA_TRY(cudaEventRecord(c->ev_d2h_data[s], c->sC));
         if (c->m >= 2) {
@@ -1216,8 +1288,12 @@ extern "C" int ckpt_snapshot(ckpt_ctx *c, uint64_t bucket_bytes, void *stream, u
                 CUDA_TRY(cudaStreamWaitEvent(o->sP, o->ev_capture, 0));
                 if (o->opt.flags & CKPT_OPT_TIMING) CUDA_TRY(cudaEventRecord(o->ev_t0, o->sP));
             }
-            for (uint64_t k = 0; k < c->op_NB; ++k) {
+            const bool one = single_launch(c);
+            if (one)
                 for (uint32_t j = 0; j < c->m; ++j)
+                    if ((rc = set_dev(c->members[j])) || (rc = issue_pack_all(c->members[j]))) goto bad;
+            for (uint64_t k = 0; k < c->op_NB; ++k) {
+                for (uint32_t j = 0; j < c->m && !one; ++j)
                     if ((rc = set_dev(c->members[j])) || (rc = stage_pack(c->members[j], k))) goto bad;
                 for (uint32_t j = 0; j < c->m; ++j)
                     if ((rc = set_dev(c->members[j])) || (rc = stage_xor(c->members[j], k))) goto bad;
@@ -1240,8 +1316,13 @@ extern "C" int ckpt_snapshot(ckpt_ctx *c, uint64_t bucket_bytes, void *stream, u
         return rc;
     }
     if ((rc = begin_member(c, caller, B))) return rc;
+    const bool one = single_launch(c);
+    if (one && (rc = issue_pack_all(c))) {
+        make_sticky(c, rc);
+        return rc;
+    }
     for (uint64_t k = 0; k < c->op_NB; ++k) {
-        if ((rc = stage_pack(c, k)) || (rc = stage_xor(c, k)) || (rc = stage_copy(c, k))) {
+        if ((!one && (rc = stage_pack(c, k))) || (rc = stage_xor(c, k)) || (rc = stage_copy(c, k))) {
             make_sticky(c, rc);
             return rc;
         }
@@ -1295,7 +1376,7 @@ static int sync_stream_timeout(ckpt_ctx *c, cudaStream_t s, const char *what) {
                 for (uint32_t j = 0; j < c->m && o < (int)sizeof buf; ++j)
                     o += snprintf(buf + o, sizeof buf - o, "%u%s", f[st * kFlagStride + j], j + 1 < c->m ? "," : "]");
             }
-            cudaMemset(c->flags, 0x7f, kFlagBytes);
+            cudaMemset(c->flags, 0x7f, kFlagAlloc);
             cudaGetLastError();
             return fail(CKPT_EPEER, "%s: timed out after %.0f s waiting for peers (member %u: %s)", what, limit, c->me, buf);
         }
