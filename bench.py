@@ -36,8 +36,8 @@ def parse():
     p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
     p.add_argument("--config", default="c2_7b_tp8")
-    p.add_argument("--bucket", type=int, default=64 << 20)
-    p.add_argument("--n-slots", type=int, default=4)
+    p.add_argument("--bucket", type=int, default=256 << 20)
+    p.add_argument("--n-slots", type=int, default=0, help="0 = full device copy (single-launch pack)")
     p.add_argument("--unit", type=int, default=64 << 10)
     p.add_argument("--pack", default="lsu", choices=["lsu", "tma", "ce"],
                    help="pack kernel: 128-bit LSU, TMA bulk through SMEM, or copy engines (zero SMs)")
@@ -313,7 +313,22 @@ def main():
     # co-running bf16 GEMM (the O_in-mem analog, P.234; HAS layer 2, P.423)
     corun = None
     if not a.no_corun:
-        corun = gemm_corun(torch, C, ctx, stream, a.bucket, barrier, allmax, dev)
+        corun = {"this_config": gemm_corun(torch, C, ctx, stream, a.bucket, barrier, allmax, dev)}
+        if a.pack != "ce" and not a.device_only:
+            # the zero-SM configuration a training job would use while GEMMs run: copy-engine
+            # pack (+ copy-engine gather of the peer units when protected)
+            o2 = C.ckpt_options_default(n_slots=a.n_slots, bucket_bytes=a.bucket, stripe_unit=a.unit,
+                                        flags=C.CKPT_OPT_TIMING | C.CKPT_OPT_CE_PACK
+                                        | (C.CKPT_OPT_CE_GATHER if world > 1 else 0))
+            ctx2 = C.ckpt_create(local, o2)
+            C.ckpt_register(ctx2, descriptors(ts, specs))
+            if world > 1:
+                C.protect_ipc(ctx2)
+            else:
+                C.ckpt_protect(ctx2, 1, 0)
+            corun["ce_pack"] = gemm_corun(torch, C, ctx2, stream, a.bucket, barrier, allmax, dev)
+            C.ckpt_destroy(ctx2)
+        corun["slowdown_pct"] = min(v["slowdown_pct"] for v in corun.values())
 
     # e2e through the public API: load (H2D of the completed image into the tensors)
     # + snapshot + commit (D2H), host wall clock, max over ranks
@@ -411,7 +426,7 @@ def gemm_corun(torch, C, ctx, stream, bucket, barrier, allmax, dev):
         return allmax(s0.elapsed_time(s1)), snap
 
     alone, withs, snaps = [], [], []
-    for _ in range(3):
+    for _ in range(5):
         alone.append(window(False)[0])
         w, s = window(True)
         withs.append(w)
@@ -423,7 +438,7 @@ def gemm_corun(torch, C, ctx, stream, bucket, barrier, allmax, dev):
             "gemm_tflops_alone": round(flops / ta / 1e9, 1),
             "snapshot_ms_while_corunning": round(statistics.median(snaps), 3),
             "snapshot_ms_alone": round(snap_ms, 3),
-            "window": "whole GEMM window (>= 1.5x snapshot), median of 3 interleaved A/B, max over ranks"}
+            "window": "whole GEMM window (>= 1.5x snapshot), median of 5 interleaved A/B, max over ranks"}
 
 
 if __name__ == "__main__":

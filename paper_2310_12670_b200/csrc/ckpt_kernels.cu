@@ -223,7 +223,7 @@ __device__ __forceinline__ void copy_chunks(const PackArgs &a, uint64_t cb, uint
     }
 }
 
-__global__ void __launch_bounds__(kPackThreads) pack_kernel(const PackArgs a) {
+__global__ void __launch_bounds__(kPackThreads, 2) pack_kernel(const PackArgs a) {
     uint64_t cb, ce;
     cta_chunk_range(a, cb, ce);
     copy_chunks(a, cb, ce);
@@ -233,7 +233,19 @@ __device__ __forceinline__ void st_release_sys(uint32_t *p, uint32_t v) {
     asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
-__global__ void __launch_bounds__(kPackThreads) pack_all_kernel(const PackAllArgs g) {
+// Publish bucket k: count this CTA's `cnt` finished groups; the CTA completing the
+// bucket stores its flag (release, system scope) locally and into every peer's page.
+__device__ __noinline__ void publish_bucket(const PackAllArgs &g, uint32_t k, uint32_t cnt, uint32_t need) {
+    __threadfence();  // this CTA's stores (ordered by the preceding barrier) before the count
+    if (atomicAdd(&g.counters[k], cnt) + cnt == need) {
+        const uint32_t v = g.seq_base + k + 1;
+        const uint32_t i = v % g.maxb;
+        st_release_sys(g.ready_local + i, v);
+        for (int p = 0; p < g.npeers; ++p) st_release_sys(g.ready_peer[p] + i, v);
+    }
+}
+
+__global__ void __launch_bounds__(kPackThreads, 2) pack_all_kernel(const __grid_constant__ PackAllArgs g) {
     PackArgs a;
     a.chunks = g.chunks;
     a.tile_first = g.tile_first;
@@ -241,28 +253,26 @@ __global__ void __launch_bounds__(kPackThreads) pack_all_kernel(const PackAllArg
     a.bucket_end = g.L;
     a.slot = g.image;
     a.unpack = 0;
-    const uint64_t ntiles = (g.L + kTile - 1) / kTile;
-    const uint64_t ngroups = (g.L + kGroup - 1) / kGroup;
-    const uint64_t tiles_per_group = kGroup / kTile;
-    for (uint64_t grp = blockIdx.x; grp < ngroups; grp += gridDim.x) {
-        const uint64_t t0 = grp * tiles_per_group;
-        const uint64_t t1 = t0 + tiles_per_group < ntiles ? t0 + tiles_per_group : ntiles;
-        copy_chunks(a, g.tile_first[t0], g.tile_first[t1]);  // ends with __syncthreads()
-        if (threadIdx.x == 0) {
-            __threadfence();  // the CTA's stores (ordered by the barrier) before the count
-            const uint64_t k = grp * kGroup / g.bucket;
-            const uint64_t lo = k * g.bucket;
-            const uint64_t hi = lo + g.bucket < g.L ? lo + g.bucket : g.L;
-            const uint32_t need = (uint32_t)((hi - lo + kGroup - 1) / kGroup);
-            if (atomicAdd(&g.counters[k], 1u) + 1 == need) {
-                __threadfence_system();
-                const uint32_t v = g.seq_base + (uint32_t)k + 1;
-                const uint32_t i = v % g.maxb;
-                st_release_sys(g.ready_local + i, v);
-                for (int p = 0; p < g.npeers; ++p) st_release_sys(g.ready_peer[p] + i, v);
-            }
+    const uint32_t ntiles = (uint32_t)((g.L + kTile - 1) / kTile);
+    const uint32_t ngroups = (uint32_t)((g.L + kGroup - 1) / kGroup);
+    const uint32_t gpb = (uint32_t)(g.bucket / kGroup);  // groups per bucket
+    constexpr uint32_t tpg = (uint32_t)(kGroup / kTile);
+    // Completion accounting batched per bucket: a CTA's groups of bucket k are consecutive
+    // in its walk, so it publishes once per bucket it touched.
+    uint32_t cur = 0, pending = 0;
+    for (uint32_t grp = blockIdx.x; grp < ngroups; grp += gridDim.x) {
+        const uint32_t k = grp / gpb;
+        if (threadIdx.x == 0 && pending && k != cur) {
+            publish_bucket(g, cur, pending, min(gpb, ngroups - cur * gpb));
+            pending = 0;
         }
+        cur = k;
+        const uint32_t t0 = grp * tpg;
+        const uint32_t t1 = t0 + tpg < ntiles ? t0 + tpg : ntiles;
+        copy_chunks(a, g.tile_first[t0], g.tile_first[t1]);  // ends with __syncthreads()
+        ++pending;
     }
+    if (threadIdx.x == 0 && pending) publish_bucket(g, cur, pending, min(gpb, ngroups - cur * gpb));
 }
 
 // ---------------------------------------------------------------------------------

@@ -1059,6 +1059,7 @@ static int issue_pack_all(ckpt_ctx *c) {
     if ((rc = timed_end(t, c->sP))) return rc;
     c->st.pack_launches++;
     c->st.pack_bytes += 2 * c->L;
+    CUDA_TRY(cudaEventRecord(c->ev_pack_all, c->sP));
     if (c->transport == CKPT_GROUP_LOCAL && c->m >= 2) {
         for (uint64_t k = 0; k < nb_data; ++k) {
             CUDA_TRY(cudaEventRecord(c->ev_packed[slot_of(c, k)], c->sP));
@@ -1189,7 +1190,10 @@ static int stage_xor(ckpt_ctx *c, uint64_t k) {
         CUDA_TRY(cudaEventRecord(c->ev_xored[s], c->sX));
         return CKPT_OK;
     }
-    // row me reads only the peers' units: no wait on this rank's own pack
+    // Row me reads only the peers' units.  After a single-launch pack the XOR also waits
+    // for this rank's own pack: the two would otherwise split HBM/NVLink bandwidth while
+    // the parity is not on the critical path (its D2H is queued after all the data).
+    if (single_launch(c) && k == 0) CUDA_TRY(cudaStreamWaitEvent(c->sX, c->ev_pack_all, 0));
     if ((rc = wait_all(c, c->sX, kReady, bucket_seq(c, k), s))) return rc;
     if (ring_reuse(c, k)) CUDA_TRY(cudaStreamWaitEvent(c->sX, c->ev_d2h_par[s], 0));
     if ((rc = do_encode(c, k, c->sX))) return rc;
@@ -1197,8 +1201,11 @@ static int stage_xor(ckpt_ctx *c, uint64_t k) {
     return sig_signal(c, c->sX, kRel, bucket_seq(c, k), s);
 }
 
-// Stage 3: copy-engine D2H of data and parity into the ongoing host image.
-static int stage_copy(ckpt_ctx *c, uint64_t k) {
+// Stage 3: copy-engine D2H of data and parity into the ongoing host image.  With
+// full-copy staging all data buckets are queued before any parity bucket (parity is
+// ready long before the data stream reaches it); the ring interleaves them per slot.
+static int stage_copy_parity(ckpt_ctx *c, uint64_t k);
+static int stage_copy(ckpt_ctx *c, uint64_t k, bool with_parity = true) {
     const uint32_t s = slot_of(c, k);
     const uint64_t bb = bucket_begin(c, k), be = bucket_end(c, k);
     const uint64_t v = valid_in_bucket(c->L, bb, be);
@@ -1214,25 +1221,28 @@ static int stage_copy(ckpt_ctx *c, uint64_t k) {
     }
     if (device_only(c)) {  // the image stays in HBM: only order the completion events
         CUDA_TRY(cudaEventRecord(c->ev_d2h_data[s], c->sC));
-        if (c->m >= 2) {
-            CUDA_TRY(cudaStreamWaitEvent(c->sC, c->ev_xored[s], 0));
-            CUDA_TRY(cudaEventRecord(c->ev_d2h_par[s], c->sC));
-        }
-        return CKPT_OK;
+        return with_parity ? stage_copy_parity(c, k) : CKPT_OK;
     }
     if (v) {
         CUDA_TRY(cudaMemcpyAsync(c->hdata[c->ongoing].p + bb, slot_ptr(c, c->staging, k), v, cudaMemcpyDeviceToHost, c->sC));
         c->st.d2h_bytes += v;
     }
     CUDA_TRY(cudaEventRecord(c->ev_d2h_data[s], c->sC));
-    if (c->m >= 2) {
-        const uint64_t pb = (be - bb) / (c->m - 1);
-        CUDA_TRY(cudaStreamWaitEvent(c->sC, c->ev_xored[s], 0));
+    return with_parity ? stage_copy_parity(c, k) : CKPT_OK;
+}
+
+static int stage_copy_parity(ckpt_ctx *c, uint64_t k) {
+    if (c->m < 2) return CKPT_OK;
+    const uint32_t s = slot_of(c, k);
+    const uint64_t bb = bucket_begin(c, k), be = bucket_end(c, k);
+    const uint64_t pb = (be - bb) / (c->m - 1);
+    CUDA_TRY(cudaStreamWaitEvent(c->sC, c->ev_xored[s], 0));
+    if (!device_only(c)) {
         CUDA_TRY(cudaMemcpyAsync(c->hpar[c->ongoing].p + bb / (c->m - 1), parity_slot_ptr(c, k), pb,
                                  cudaMemcpyDeviceToHost, c->sC));
         c->st.d2h_bytes += pb;
-        CUDA_TRY(cudaEventRecord(c->ev_d2h_par[s], c->sC));
     }
+    CUDA_TRY(cudaEventRecord(c->ev_d2h_par[s], c->sC));
     return CKPT_OK;
 }
 
@@ -1298,8 +1308,11 @@ extern "C" int ckpt_snapshot(ckpt_ctx *c, uint64_t bucket_bytes, void *stream, u
                 for (uint32_t j = 0; j < c->m; ++j)
                     if ((rc = set_dev(c->members[j])) || (rc = stage_xor(c->members[j], k))) goto bad;
                 for (uint32_t j = 0; j < c->m; ++j)
-                    if ((rc = set_dev(c->members[j])) || (rc = stage_copy(c->members[j], k))) goto bad;
+                    if ((rc = set_dev(c->members[j])) || (rc = stage_copy(c->members[j], k, !c->full_copy))) goto bad;
             }
+            for (uint64_t k = 0; c->full_copy && k < c->op_NB; ++k)
+                for (uint32_t j = 0; j < c->m; ++j)
+                    if ((rc = set_dev(c->members[j])) || (rc = stage_copy_parity(c->members[j], k))) goto bad;
             for (uint32_t j = 0; j < c->m; ++j) {
                 ckpt_ctx *o = c->members[j];
                 if ((rc = set_dev(o)) || (rc = stage_finish(o))) goto bad;
@@ -1322,7 +1335,13 @@ extern "C" int ckpt_snapshot(ckpt_ctx *c, uint64_t bucket_bytes, void *stream, u
         return rc;
     }
     for (uint64_t k = 0; k < c->op_NB; ++k) {
-        if ((!one && (rc = stage_pack(c, k))) || (rc = stage_xor(c, k)) || (rc = stage_copy(c, k))) {
+        if ((!one && (rc = stage_pack(c, k))) || (rc = stage_xor(c, k)) || (rc = stage_copy(c, k, !c->full_copy))) {
+            make_sticky(c, rc);
+            return rc;
+        }
+    }
+    for (uint64_t k = 0; c->full_copy && k < c->op_NB; ++k) {
+        if ((rc = stage_copy_parity(c, k))) {
             make_sticky(c, rc);
             return rc;
         }

@@ -208,11 +208,12 @@ def test_bucket_size_invariance_and_commit(torch, C):
     """I8: images do not depend on the bucket size; commit keeps the previous image
     readable until the next snapshot is waited (P.553-554, S.431)."""
     from synth.gpu import fill_state
+    # full-copy staging rounds buckets to lcm(stripe, 64 KiB) = 192 KiB here
     states, ctxs = make_group(torch, C, 4, 4096, n_slots=0)
     try:
-        snapshot_group(C, ctxs, bucket=3 * 4096)
+        snapshot_group(C, ctxs, bucket=3 * 65536)
         first = [tuple(x.copy() for x in C.ckpt_host_view(c, 0, copy=True)) for c in ctxs]
-        snapshot_group(C, ctxs, bucket=3 * 4096 * 7)
+        snapshot_group(C, ctxs, bucket=3 * 65536 * 3)
         for c, (d0, p0) in zip(ctxs, first):
             d, p = C.ckpt_host_view(c, 0, copy=True)
             assert_bytes_equal(d, d0, "data vs bucket size")
@@ -337,3 +338,22 @@ def test_device_only_drill(torch, C, m, unit, flags):
     finally:
         for c in ctxs:
             C.ckpt_destroy(c)
+
+
+def test_ring_bucket_sizes_match_full_copy(torch, C):
+    """I8 across staging modes: ring slots with 4 different bucket sizes give the same
+    images as the full-copy single-launch pack."""
+    ref = None
+    for n_slots, bucket in [(0, 1 << 20), (2, 12288), (3, 12288 * 5), (2, 12288 * 40)]:
+        states, ctxs = make_group(torch, C, 4, 4096, n_slots=n_slots, bucket=max(bucket, 4096))
+        try:
+            snapshot_group(C, ctxs, bucket=bucket)
+            imgs = [C.ckpt_host_view(c, 0, copy=True) for c in ctxs]
+        finally:
+            for c in ctxs:
+                C.ckpt_destroy(c)
+        if ref is None:
+            ref = imgs
+        for j, ((d, p), (d0, p0)) in enumerate(zip(imgs, ref)):
+            assert_bytes_equal(d, d0, f"rank {j} data, slots={n_slots} bucket={bucket}")
+            assert_bytes_equal(p, p0, f"rank {j} parity, slots={n_slots} bucket={bucket}")

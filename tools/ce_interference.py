@@ -48,4 +48,4 @@ for bucket in (64 << 20, 256 << 20):
         res[f"B{bucket >> 20}M_{cond}"] = {"pack_ms": round(ms, 3),
                                            "pack_gbs": round(st["pack_bytes"] / st["pack_launches"] / ms / 1e6, 1)}
     C.ckpt_destroy(ctx)
-print(json.dumps(res, indent=0))
+print(json.dumps(res))
