@@ -36,7 +36,7 @@ def parse():
     p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
     p.add_argument("--config", default="c2_7b_tp8")
-    p.add_argument("--bucket", type=int, default=256 << 20)
+    p.add_argument("--bucket", type=int, default=1 << 30)
     p.add_argument("--n-slots", type=int, default=0, help="0 = full device copy (single-launch pack)")
     p.add_argument("--unit", type=int, default=64 << 10)
     p.add_argument("--pack", default="lsu", choices=["lsu", "tma", "ce"],

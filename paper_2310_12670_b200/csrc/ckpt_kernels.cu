@@ -236,7 +236,9 @@ __device__ __forceinline__ void st_release_sys(uint32_t *p, uint32_t v) {
 // Publish bucket k: count this CTA's `cnt` finished groups; the CTA completing the
 // bucket stores its flag (release, system scope) locally and into every peer's page.
 __device__ __noinline__ void publish_bucket(const PackAllArgs &g, uint32_t k, uint32_t cnt, uint32_t need) {
-    __threadfence();  // this CTA's stores (ordered by the preceding barrier) before the count
+    // this CTA's stores (ordered by the preceding barrier) before the count: acq_rel at
+    // gpu scope is enough here (__threadfence is the heavier fence.sc)
+    asm volatile("fence.acq_rel.gpu;" ::: "memory");
     if (atomicAdd(&g.counters[k], cnt) + cnt == need) {
         const uint32_t v = g.seq_base + k + 1;
         const uint32_t i = v % g.maxb;

@@ -923,9 +923,13 @@ static int do_pack(ckpt_ctx *c, uint64_t k, uint8_t *slot, cudaStream_t s, bool 
     return CKPT_OK;
 }
 
-// Encode row r = c->me for bucket k (Eq 1): terms are every peer j's data slot.
+// Encode row r = c->me over image bytes [bb, be) (Eq 1): terms are every peer j's data
+// slot.  k is the bucket holding bb (a full-copy encode may span every bucket).
+static int do_encode_range(ckpt_ctx *c, uint64_t k, uint64_t bb, uint64_t be, cudaStream_t s);
 static int do_encode(ckpt_ctx *c, uint64_t k, cudaStream_t s) {
-    const uint64_t bb = bucket_begin(c, k), be = bucket_end(c, k);
+    return do_encode_range(c, k, bucket_begin(c, k), bucket_end(c, k), s);
+}
+static int do_encode_range(ckpt_ctx *c, uint64_t k, uint64_t bb, uint64_t be, cudaStream_t s) {
     const uint64_t stripe = (uint64_t)(c->m - 1) * c->unit;
     XorArgs a;
     memset(&a, 0, sizeof a);
@@ -1174,8 +1178,28 @@ static int do_encode_gathered(ckpt_ctx *c, uint64_t k, cudaStream_t s) {
 }
 
 // Stage 2: parity of bucket k once every member's pack(k) is visible, then REL.
+// Full-copy staging after a single-launch pack: ONE XOR launch over the whole image once
+// this rank's pack is done and every peer published every bucket (parity is not on the
+// critical path: its D2H is queued after all the data).  Per-bucket events keep the
+// parity D2H ordering uniform.
+static int stage_xor_all(ckpt_ctx *c) {
+    int rc;
+    CUDA_TRY(cudaStreamWaitEvent(c->sX, c->ev_pack_all, 0));
+    for (uint64_t k = 0; k < c->op_NB; ++k)
+        if ((rc = wait_all(c, c->sX, kReady, bucket_seq(c, k), slot_of(c, k)))) return rc;
+    if ((rc = do_encode_range(c, 0, 0, c->Lstar, c->sX))) return rc;
+    for (uint64_t k = 0; k < c->op_NB; ++k) CUDA_TRY(cudaEventRecord(c->ev_xored[slot_of(c, k)], c->sX));
+    // REL is a monotonic scalar: one signal covers every bucket
+    return sig_signal(c, c->sX, kRel, bucket_seq(c, c->op_NB - 1), slot_of(c, c->op_NB - 1));
+}
+
+static bool xor_in_one_launch(const ckpt_ctx *c) {
+    return c->m >= 2 && single_launch(c) && !(c->opt.flags & CKPT_OPT_CE_GATHER);
+}
+
 static int stage_xor(ckpt_ctx *c, uint64_t k) {
     if (c->m < 2) return CKPT_OK;
+    if (xor_in_one_launch(c)) return k + 1 == c->op_NB ? stage_xor_all(c) : CKPT_OK;
     const uint32_t s = slot_of(c, k);
     int rc;
     if (c->opt.flags & CKPT_OPT_CE_GATHER) {

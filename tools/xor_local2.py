@@ -22,6 +22,7 @@ def main():
     p.add_argument("--reps", type=int, default=3)
     p.add_argument("--bucket", type=int, default=64 << 20)
     p.add_argument("--flags", type=int, default=0)
+    p.add_argument("--with-d2h", action="store_true", help="run a pinned D2H on every device meanwhile")
     a = p.parse_args()
     import torch
 
@@ -39,7 +40,16 @@ def main():
         ctxs.append(c)
         states.append((specs, ts))
     C.protect_local(ctxs)
+    side, hbs, dbs = [], [], []
+    if a.with_d2h:
+        for j in range(m):
+            side.append(torch.cuda.Stream(device=j))
+            hbs.append(torch.empty(4 << 30, dtype=torch.uint8, pin_memory=True))
+            dbs.append(torch.empty(4 << 30, dtype=torch.uint8, device=f"cuda:{j}"))
     for r in range(a.reps + 1):
+        for j in range(len(side)):
+            with torch.cuda.stream(side[j]):
+                hbs[j].copy_(dbs[j], non_blocking=True)
         if r == 1:
             for c in ctxs:
                 C.ckpt_stats_reset(c)
