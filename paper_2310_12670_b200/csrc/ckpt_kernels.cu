@@ -494,12 +494,14 @@ cudaError_t launch_pack(const PackArgs &a, int max_ctas, cudaStream_t s, bool tm
     if (a.bucket_end <= a.bucket_begin) return cudaSuccess;
     const uint64_t ntiles = (a.bucket_end + kTile - 1) / kTile - a.bucket_begin / kTile;
     if (tma) {
-        static bool attr_set = false;  // per process; the attribute is per function
+        static unsigned long long attr_set = 0;  // bit d: attribute set on device d
         const int smem = kTmaStages * kTmaStage;
-        if (!attr_set) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        if (!(attr_set & (1ull << dev))) {
             cudaError_t e = cudaFuncSetAttribute(pack_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
             if (e != cudaSuccess) return e;
-            attr_set = true;
+            attr_set |= 1ull << dev;
         }
         // 3 CTAs of 64 KiB SMEM per SM: 1.5x the LSU CTA budget
         const uint64_t cap = (uint64_t)max_ctas * 3 / 2;

@@ -40,3 +40,18 @@ def assert_bytes_equal(got, want, what):
         bad = np.nonzero(got != want)[0]
         raise AssertionError(f"{what}: {bad.size} bytes differ, first at {bad[0]} "
                              f"(got {got[bad[0]]:#x} want {want[bad[0]]:#x})")
+
+
+def image_slice(specs, rank, off, n, seed=synth.SEED, align=256):
+    """Bytes [off, off+n) of rank's packed image, computed from the oracle's layout rule and
+    the oracle's generator copy only (for sampled checks at full size)."""
+    offs, L = oracle.layout([s.nbytes for s in specs], align)
+    out = np.zeros(n, np.uint8)
+    import bisect
+    t = max(0, bisect.bisect_right(offs, off) - 1)
+    while t < len(specs) and offs[t] < off + n:
+        lo, hi = max(off, offs[t]), min(off + n, offs[t] + specs[t].nbytes)
+        if lo < hi:
+            out[lo - off:hi - off] = oracle.fill(seed, rank, t, hi - lo, lo - offs[t])
+        t += 1
+    return out

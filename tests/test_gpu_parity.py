@@ -357,3 +357,43 @@ def test_ring_bucket_sizes_match_full_copy(torch, C):
         for j, ((d, p), (d0, p0)) in enumerate(zip(imgs, ref)):
             assert_bytes_equal(d, d0, f"rank {j} data, slots={n_slots} bucket={bucket}")
             assert_bytes_equal(p, p0, f"rank {j} parity, slots={n_slots} bucket={bucket}")
+
+
+@pytest.mark.parametrize("n_slots,m", [(0, 1), (2, 1), (0, 3), (3, 3)])
+def test_fence_and_capture_point(torch, C, n_slots, m):
+    """Q10: the snapshot holds the tensors as of the caller stream's position at
+    ckpt_snapshot; after ckpt_fence the caller may mutate them on that stream while the
+    D2H is still running, and the committed image is unaffected."""
+    from synth.gpu import fill_state
+    states = [tiny(j, n=7) for j in range(m)]
+    ctxs = [make_ctx(C, st, n_slots=n_slots, bucket_bytes=12288 if n_slots else 1 << 20, stripe_unit=4096)
+            for st in states]
+    s = torch.cuda.Stream()
+    try:
+        if m == 1:
+            C.ckpt_protect(ctxs[0], 1, 0)
+        else:
+            C.protect_local(ctxs)
+        with torch.cuda.stream(s):
+            # enqueued BEFORE the snapshot on the same stream: must be captured
+            for j, (_, ts) in enumerate(states):
+                fill_state(ts, j, seed=5, xor_mode=1, stream=s)
+            ids = [C.ckpt_snapshot(c, 0, s) for c in ctxs]
+            for c, i in zip(ctxs, ids):
+                C.ckpt_fence(c, i, s)
+            # enqueued AFTER the fence: must NOT be captured
+            for j, (_, ts) in enumerate(states):
+                fill_state(ts, j, seed=6, xor_mode=1, stream=s)
+        for c, i in zip(ctxs, ids):
+            C.ckpt_wait(c, i)
+        for j, ((specs, _), c) in enumerate(zip(states, ctxs)):
+            want = []
+            for t, sp in enumerate(specs):
+                w = oracle.fill(synth.SEED, j, t, sp.nbytes) ^ oracle.fill(5, j, t, sp.nbytes)
+                want.append(w)
+            off, L = oracle.layout([sp.nbytes for sp in specs])
+            d, _ = C.ckpt_host_view(c, 0, copy=True)
+            assert_bytes_equal(d[:L], oracle.pack(want, off, L), f"rank {j} image at the capture point")
+    finally:
+        for c in ctxs:
+            C.ckpt_destroy(c)

@@ -147,3 +147,81 @@ def test_ipc_group_pair():
 
 def test_ipc_c1_16mib_all_gpus():
     _run(min(_world(), 8), ("c1_16mb_fp32_m8", 65536, 0, 64 << 20, 0, 0))
+
+
+def _worker_c2(rank, world, port, q):
+    try:
+        os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank), WORLD_SIZE=str(world))
+        import torch
+        import torch.distributed as dist
+
+        import oracle
+        import synth
+        from gpu_util import image_slice
+        from paper_2310_12670_b200 import ckpt as C
+        from synth.gpu import descriptors, make_rank_state
+
+        torch.cuda.set_device(rank)
+        dev = torch.device("cuda", rank)
+        dist.init_process_group("nccl", device_id=dev)
+        specs, ts = make_rank_state("c2_7b_tp8", rank, dev)
+        ctx = C.ckpt_create(rank, C.ckpt_options_default(n_slots=0, bucket_bytes=1 << 30))  # bench defaults
+        C.ckpt_register(ctx, descriptors(ts, specs))
+        C.protect_ipc(ctx)
+        g = C.ckpt_geometry(ctx)
+        sid = C.ckpt_snapshot(ctx)
+        C.ckpt_wait(ctx, sid)
+        d, p = C.ckpt_host_view(ctx, 0)
+        u, m = g["unit"], g["m"]
+        stripe = (m - 1) * u
+        nst = g["L_star"] // stripe
+        rng = np.random.default_rng(rank)
+        ok = []
+        all_specs = [synth.config_tensors("c2_7b_tp8", j) for j in range(m)]
+        for s in [0, nst - 1] + rng.integers(0, nst, 6).tolist():
+            imgs = [image_slice(all_specs[j], j, s * stripe, stripe) for j in range(m)]
+            want = oracle.encode(imgs, u, rank)
+            ok.append(bool(np.array_equal(p[s * u:(s + 1) * u].copy(), want)))
+            ok.append(bool(np.array_equal(d[s * stripe:(s + 1) * stripe].copy(), imgs[rank])))
+        del d, p
+        C.ckpt_destroy(ctx)
+        dist.barrier()
+        dist.destroy_process_group()
+        q.put((rank, ok, None))
+    except Exception:
+        q.put((rank, None, traceback.format_exc()))
+
+
+def test_ipc_c2_7b_full_size_sampled():
+    """BASELINE config 2 at full size in the bench launch configuration (one process per
+    GPU, full-copy staging, 1 GiB buckets): sampled stripes of data and parity of every
+    rank against the oracle."""
+    world = min(_world(), 8)
+    import queue
+    import time
+
+    import torch.multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    ps = [ctx.Process(target=_worker_c2, args=(r, world, port, q)) for r in range(world)]
+    for p in ps:
+        p.start()
+    res, t0 = [], time.time()
+    try:
+        while len(res) < world:
+            try:
+                r = q.get(timeout=5)
+            except queue.Empty:
+                assert all(p.exitcode in (None, 0) for p in ps), "worker died"
+                assert time.time() - t0 < 600, "timed out"
+                continue
+            assert r[2] is None, r[2]
+            res.append(r)
+    finally:
+        for p in ps:
+            p.join(30)
+            if p.is_alive():
+                p.kill()
+    for rank, ok, _ in res:
+        assert all(ok), (rank, ok)
