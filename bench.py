@@ -233,20 +233,23 @@ def main():
     m = g["m"]
     stream = torch.cuda.current_stream()
 
-    # host-link roofline, measured live: pinned D2H of 1 GiB, all ranks at once
-    hb = torch.empty(1 << 30, dtype=torch.uint8, pin_memory=True)
-    db = torch.empty(1 << 30, dtype=torch.uint8, device=dev)
+    # host-link roofline, measured live: pinned D2H of 4 GiB by every rank at once
+    # (barrier-aligned; the slowest rank's rate is what a synchronous step can get)
+    nprobe = 4 << 30
+    hb = torch.empty(nprobe, dtype=torch.uint8, pin_memory=True)
+    db = torch.empty(nprobe, dtype=torch.uint8, device=dev)
     best = 0.0
-    barrier()
     for _ in range(3):
+        barrier()
+        torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
         hb.copy_(db, non_blocking=True)
         e1.record()
         e1.synchronize()
-        best = max(best, (1 << 30) / e0.elapsed_time(e1) / 1e6)
+        best = max(best, nprobe / e0.elapsed_time(e1) / 1e6)
     d2h_peak = best
-    del db
+    del db, hb
 
     def step():
         sid = C.ckpt_snapshot(ctx, a.bucket, stream)

@@ -81,16 +81,18 @@ def main():
             dt = amax(time.perf_counter() - t0)
             if r:
                 times.append(dt)
+            else:
+                C.ckpt_stats_reset(ctx)  # the first snapshot pays first-touch of peer mappings
         st = C.ckpt_get_stats(ctx)
         t = statistics.median(times)
         rec = {"config": a.config, "m": g["m"], "bucket_mib": bmib, "n_slots": n_slots, "flags": flags,
                "state_bytes": S, "L_star": g["L_star"], "snapshot_ms": round(t * 1e3, 3),
-               "state_gbs_per_gpu": round(S / t / 1e9, 3), "wire_gbs_per_gpu": round(st["d2h_bytes"] / (a.reps + 1) / t / 1e9, 3),
+               "state_gbs_per_gpu": round(S / t / 1e9, 3), "wire_gbs_per_gpu": round(st["d2h_bytes"] / a.reps / t / 1e9, 3),
                "pack_us_per_launch": round(st["pack_ms"] / max(st["pack_launches"], 1) * 1e3, 2),
                "xor_us_per_launch": round(st["xor_ms"] / max(st["xor_launches"], 1) * 1e3, 2),
                "pack_hbm_gbs": round(st["pack_bytes"] / max(st["pack_ms"], 1e-9) / 1e6, 1),
                "xor_nvlink_gbs": round(st["xor_bytes_in"] / max(st["xor_ms"], 1e-9) / 1e6, 1),
-               "launches_per_snapshot": (st["pack_launches"] + st["xor_launches"]) // (a.reps + 1)}
+               "launches_per_snapshot": (st["pack_launches"] + st["xor_launches"]) // a.reps}
         if a.drill and g["m"] >= 2:
             lost = [int(x) for x in a.lost.split(",")] if a.lost else [0, g["m"] - 1]
             for k in lost:
