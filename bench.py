@@ -45,6 +45,7 @@ def parse():
                    help="parity: XOR kernel reads peers over NVLink, or copy engines pull units first")
     p.add_argument("--device-only", action="store_true",
                    help="CKPT_OPT_DEVICE_ONLY: device-side protect only (pack + parity into HBM, no D2H)")
+    p.add_argument("--max-ctas", type=int, default=0, help="CTA budget of a pack/XOR launch (0 = 2 x SMs)")
     p.add_argument("--no-corun", action="store_true", help="skip the co-running GEMM measurement")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu-baseline", action="store_true")
@@ -217,7 +218,8 @@ def main():
              | (C.CKPT_OPT_DEVICE_ONLY if a.device_only else 0))
     if a.device_only:
         a.n_slots = 0
-    opts = C.ckpt_options_default(n_slots=a.n_slots, bucket_bytes=a.bucket, stripe_unit=a.unit, flags=flags)
+    opts = C.ckpt_options_default(n_slots=a.n_slots, bucket_bytes=a.bucket, stripe_unit=a.unit, flags=flags,
+                                  max_ctas=a.max_ctas)
     ctx = C.ckpt_create(local, opts)
     t_setup = time.perf_counter()
     C.ckpt_register(ctx, descriptors(ts, specs), {"rank": rank, "world": world, "local_rank": local,
@@ -369,6 +371,7 @@ def main():
             "config": {"workload": a.config, "state_bytes_per_gpu": S, "tensors_per_gpu": len(specs),
                        "m": m, "L_star": g["L_star"], "stripe_unit": g["unit"], "bucket_bytes": a.bucket,
                        "n_slots": a.n_slots, "pack": a.pack, "gather": a.gather, "device_only": a.device_only,
+                       "max_ctas": a.max_ctas or "2 x SMs",
                        "l2": f"inputs {S / 1e9:.2f} GB/GPU >> 126 MB L2; no flush needed"},
             "per_gpu_gbs": round(value / N, 3),
             "host_link": None if a.device_only else {
