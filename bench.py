@@ -288,7 +288,8 @@ def main():
         kern.append(("pack", st["pack_ms"], {"bound": "hbm", "achieved": per / dur / 1e6, "peak": hbm_peak,
                                              "unit": "GB/s",
                                              "kernel": ("pack_all_kernel" if a.n_slots == 0 else "pack_kernel")
-                                             if a.pack == "lsu" else "pack_tma_kernel",
+                                             if a.pack == "lsu" else
+                                             ("pack_all_tma_kernel" if a.n_slots == 0 else "pack_tma_kernel"),
                                              "bytes_per_launch": per, "avg_launch_us": dur * 1e3,
                                              "launches": st["pack_launches"],
                                              "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy r+w)"}))

@@ -11,6 +11,8 @@
 //    for the encode: (m-1) peer units in per parity unit out.
 //
 // No tensor cores: the path is pure data movement.
+#include <cstdlib>
+
 #include "ckpt_kernels.cuh"
 
 namespace reft {
@@ -326,7 +328,11 @@ __device__ __forceinline__ void bulk_wait_read_n(uint32_t n) {
         case 0: bulk_wait_read<0>(); break;
         case 1: bulk_wait_read<1>(); break;
         case 2: bulk_wait_read<2>(); break;
-        default: bulk_wait_read<3>(); break;
+        case 3: bulk_wait_read<3>(); break;
+        case 4: bulk_wait_read<4>(); break;
+        case 5: bulk_wait_read<5>(); break;
+        case 6: bulk_wait_read<6>(); break;
+        default: bulk_wait_read<7>(); break;
     }
 }
 __device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
@@ -412,6 +418,116 @@ __global__ void __launch_bounds__(kTmaThreads) pack_tma_kernel(const PackArgs a)
     __syncwarp();
 }
 
+
+// ---------------------------------------------------------------------------------
+// TMA single-launch pack.  One elected lane per CTA drives a ring of NS SMEM stages of
+// up to 16 KiB: bulk loads (cp.async.bulk G->S, mbarrier complete_tx) run NS-1 deep and
+// every retired stage is written back with a bulk store (S->G, bulk_group).  A 32-thread
+// CTA keeps ~(NS-1) x 16 KiB in flight -- several times the LSU kernel's bytes per SM,
+// so the same HBM bandwidth costs fewer SM-seconds (the co-running GEMM loses less).
+// Bucket publication as in pack_all_kernel, after draining the CTA's bulk stores and a
+// proxy fence (async-proxy writes before the generic-proxy flag store).
+template <int NS>
+struct BulkRing {
+    uint8_t *smem;
+    uint64_t *bars;
+    uint32_t phase, issued, done;
+    Piece ring[NS];
+    __device__ __forceinline__ void retire() {
+        const uint32_t so = done % NS;
+        mbar_wait(&bars[so], (phase >> so) & 1);
+        phase ^= 1u << so;
+        bulk_s2g(ring[so].dst, smem + so * kTmaStage, ring[so].bytes);
+        bulk_commit();
+        ++done;
+    }
+    __device__ __forceinline__ void push(const uint8_t *s, uint8_t *d, uint32_t bytes) {
+        if (issued - done == NS - 1) retire();
+        const uint32_t st = issued % NS;
+        if (issued >= NS) bulk_wait_read_n(done + NS - 1 - issued);
+        ring[st] = Piece{s, d, bytes};
+        mbar_expect_tx(&bars[st], bytes);
+        bulk_g2s(smem + st * kTmaStage, s, bytes, &bars[st]);
+        ++issued;
+    }
+    __device__ __forceinline__ void drain() {
+        while (done < issued) retire();
+        bulk_wait_all();
+        asm volatile("fence.proxy.async.global;" ::: "memory");
+    }
+};
+
+template <int NS>
+__global__ void __launch_bounds__(kTmaThreads) pack_all_tma_kernel(const __grid_constant__ PackAllArgs g) {
+    extern __shared__ __align__(128) uint8_t smem[];
+    __shared__ __align__(8) uint64_t bars[NS];
+    const uint32_t lane = threadIdx.x;
+    BulkRing<NS> R;
+    R.smem = smem;
+    R.bars = bars;
+    R.phase = R.issued = R.done = 0;
+    if (lane == 0) {
+        for (int i = 0; i < NS; ++i) mbar_init(&bars[i], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    }
+    __syncwarp();
+    PackArgs a;
+    a.chunks = g.chunks;
+    a.tile_first = g.tile_first;
+    a.bucket_begin = 0;
+    a.bucket_end = g.L;
+    a.slot = g.image;
+    a.unpack = 0;
+    const uint32_t ntiles = (uint32_t)((g.L + kTile - 1) / kTile);
+    const uint32_t ngroups = (uint32_t)((g.L + kGroup - 1) / kGroup);
+    const uint32_t gpb = (uint32_t)(g.bucket / kGroup);
+    constexpr uint32_t tpg = (uint32_t)(kGroup / kTile);
+    uint32_t cur = 0, pending = 0;
+    for (uint32_t grp = blockIdx.x; grp < ngroups; grp += gridDim.x) {
+        const uint32_t k = grp / gpb;
+        if (pending && k != cur) {
+            __syncwarp();
+            if (lane == 0) {
+                R.drain();
+                publish_bucket(g, cur, pending, min(gpb, ngroups - cur * gpb));
+            }
+            pending = 0;
+        }
+        cur = k;
+        const uint32_t t0 = grp * tpg;
+        const uint32_t t1 = t0 + tpg < ntiles ? t0 + tpg : ntiles;
+        const uint32_t cb = g.tile_first[t0], ce = g.tile_first[t1];
+        for (uint32_t c = cb; c < ce; ++c) {
+            const uint8_t *src;
+            uint8_t *dst;
+            const uint64_t n = clip_chunk(a, g.chunks[c], src, dst);
+            if (n == 0) continue;
+            if (!src) {
+                block_zero(dst, n);
+                continue;
+            }
+            if ((((uintptr_t)dst ^ (uintptr_t)src) & 15) || n < 64) {
+                block_copy(dst, src, n);
+                continue;
+            }
+            const uint64_t head = (16 - ((uintptr_t)dst & 15)) & 15;
+            const uint64_t body = (n - head) & ~(uint64_t)15;
+            const uint64_t tail = n - head - body;
+            if (lane < head) dst[lane] = src[lane];
+            if (lane < tail) dst[head + body + lane] = src[head + body + lane];
+            if (lane == 0)  // chunks never exceed a 16 KiB tile: one stage each
+                R.push(src + head, dst + head, (uint32_t)body);
+        }
+        ++pending;
+    }
+    __syncwarp();
+    if (lane == 0) {
+        R.drain();
+        if (pending) publish_bucket(g, cur, pending, min(gpb, ngroups - cur * gpb));
+    }
+}
+
 // ---------------------------------------------------------------------------------
 // XOR gather.  Work is split into tiles of kXorThreads * U 16-byte words
 // inside one unit, so the stripe index needs one 32-bit division per tile.
@@ -477,9 +593,39 @@ __global__ void signal_kernel(const SignalArgs a) {
 
 }  // namespace
 
-cudaError_t launch_pack_all(const PackAllArgs &a, int max_ctas, cudaStream_t s) {
+template <int NS>
+static cudaError_t launch_pack_all_tma(const PackAllArgs &a, uint64_t ngroups, int ctas_per_sm, int sms, cudaStream_t s) {
+    static unsigned long long attr_set = 0;  // bit d: attribute set on device d
+    const int smem = NS * kTmaStage;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (!(attr_set & (1ull << dev))) {
+        cudaError_t e = cudaFuncSetAttribute(pack_all_tma_kernel<NS>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        if (e != cudaSuccess) return e;
+        attr_set |= 1ull << dev;
+    }
+    const uint64_t cap = (uint64_t)sms * ctas_per_sm;
+    const uint64_t g = ngroups < cap ? ngroups : cap;
+    pack_all_tma_kernel<NS><<<(unsigned)g, kTmaThreads, smem, s>>>(a);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_pack_all(const PackAllArgs &a, int max_ctas, cudaStream_t s, bool tma) {
     const uint64_t ngroups = (a.L + kGroup - 1) / kGroup;
     if (ngroups == 0) return cudaSuccess;
+    if (tma) {
+        // max_ctas is the LSU budget (2 per SM): the TMA kernel runs max_ctas/2 SMs with
+        // NS stages; CKPT_TMA_STAGES picks 4 (3 CTAs/SM), 6 (2/SM) or 8 (1/SM, default)
+        static int ns = -1;
+        if (ns < 0) {
+            const char *e = getenv("CKPT_TMA_STAGES");
+            ns = e ? atoi(e) : 8;
+        }
+        const int sms = max_ctas / 2 > 0 ? max_ctas / 2 : 1;
+        if (ns == 4) return launch_pack_all_tma<4>(a, ngroups, 3, sms, s);
+        if (ns == 6) return launch_pack_all_tma<6>(a, ngroups, 2, sms, s);
+        return launch_pack_all_tma<8>(a, ngroups, 1, sms, s);
+    }
     const uint64_t g = ngroups < (uint64_t)max_ctas ? ngroups : (uint64_t)max_ctas;
     pack_all_kernel<<<(unsigned)g, kPackThreads, 0, s>>>(a);
     return cudaGetLastError();

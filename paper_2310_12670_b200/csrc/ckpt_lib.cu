@@ -1029,7 +1029,7 @@ static uint64_t effective_bucket(const ckpt_ctx *c, uint64_t req) {
 }
 
 static bool single_launch(const ckpt_ctx *c) {
-    return c->full_copy && !(c->opt.flags & (CKPT_OPT_CE_PACK | CKPT_OPT_TMA_PACK)) &&
+    return c->full_copy && !(c->opt.flags & CKPT_OPT_CE_PACK) &&
            (c->transport == CKPT_GROUP_LOCAL && c->m >= 2 ? true : load_memops() == CKPT_OK);
 }
 
@@ -1059,7 +1059,7 @@ static int issue_pack_all(ckpt_ctx *c) {
     a.maxb = kMaxB;
     TimedLaunch *t;
     if ((rc = timed_begin(c, c->sP, 0, &t))) return rc;
-    CUDA_TRY(launch_pack_all(a, c->max_ctas, c->sP));
+    CUDA_TRY(launch_pack_all(a, c->max_ctas, c->sP, (c->opt.flags & CKPT_OPT_TMA_PACK) != 0));
     if ((rc = timed_end(t, c->sP))) return rc;
     c->st.pack_launches++;
     c->st.pack_bytes += 2 * c->L;
