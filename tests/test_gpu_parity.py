@@ -397,3 +397,53 @@ def test_fence_and_capture_point(torch, C, n_slots, m):
     finally:
         for c in ctxs:
             C.ckpt_destroy(c)
+
+
+@pytest.mark.parametrize("flags", [0, 0x2, 0x8])
+@pytest.mark.parametrize("n_slots", [0, 2])
+def test_no_writes_outside_tensors(torch, C, flags, n_slots):
+    """Bounds check without compute-sanitizer (closed on this pool): every tensor is a
+    view with 64..79 canary bytes on both sides inside its own allocation; snapshot,
+    rebuild and load (unpack) must leave every canary intact, for odd sizes and every
+    misalignment mod 16."""
+    from synth.gpu import descriptors, fill_state
+    m = 3
+    canary = 0x3C
+    states, bases = [], []
+    rng = np.random.default_rng(7)
+    for j in range(m):
+        specs = synth.config_tensors("tiny_9", j)
+        ts, bs = [], []
+        for i, s in enumerate(specs):
+            pre = 64 + (i * 3 + j) % 16
+            b = torch.full((pre + s.nbytes + 79,), canary, dtype=torch.uint8, device="cuda:0")
+            bs.append((b, pre))
+            ts.append(b[pre:pre + s.nbytes])
+        fill_state(ts, j)
+        states.append((specs, ts))
+        bases.append(bs)
+    ctxs = []
+    for specs, ts in states:
+        c = C.ckpt_create(0, C.ckpt_options_default(n_slots=n_slots, bucket_bytes=12288 if n_slots else 1 << 20,
+                                                    stripe_unit=4096, flags=flags))
+        C.ckpt_register(c, [C.tensor_desc(t, name=s.name) for t, s in zip(ts, specs)])
+        ctxs.append(c)
+    try:
+        C.protect_local(ctxs)
+        snapshot_group(C, ctxs)
+        C.ckpt_forget(ctxs[1])
+        for c in ctxs:
+            C.ckpt_rebuild(c, 1)
+        for j, (_, ts) in enumerate(states):
+            fill_state(ts, j, seed=3, xor_mode=1)
+        for c in ctxs:
+            C.ckpt_load(c)
+        torch.cuda.synchronize()
+        for j, (specs, ts) in enumerate(states):
+            for i, ((b, pre), s) in enumerate(zip(bases[j], specs)):
+                h = b.cpu().numpy()
+                assert (h[:pre] == canary).all() and (h[pre + s.nbytes:] == canary).all(), f"rank {j} tensor {i}"
+                assert_bytes_equal(h[pre:pre + s.nbytes], oracle.fill(synth.SEED, j, i, s.nbytes), f"rank {j} tensor {i}")
+    finally:
+        for c in ctxs:
+            C.ckpt_destroy(c)
