@@ -36,7 +36,7 @@ def parse():
     p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
     p.add_argument("--config", default="c2_7b_tp8")
-    p.add_argument("--bucket", type=int, default=1 << 30)
+    p.add_argument("--bucket", type=int, default=512 << 20)
     p.add_argument("--n-slots", type=int, default=0, help="0 = full device copy (single-launch pack)")
     p.add_argument("--unit", type=int, default=64 << 10)
     p.add_argument("--pack", default="lsu", choices=["lsu", "tma", "ce"],
@@ -218,8 +218,18 @@ def main():
              | (C.CKPT_OPT_DEVICE_ONLY if a.device_only else 0))
     if a.device_only:
         a.n_slots = 0
+    # pinned host arena: 2 x (L + L/(m-1)) per rank; fall back to one buffer if the node's
+    # available memory (all ranks together, +25% headroom) would not hold two
+    host_buffers = 2
+    try:
+        avail = int([l for l in open("/proc/meminfo") if l.startswith("MemAvailable")][0].split()[1]) * 1024
+        need = world * 2 * (S + (S // (world - 1) if world > 1 else 0)) * 1.25 + world * (4 << 30)
+        if need > avail:
+            host_buffers = 1
+    except Exception:
+        pass
     opts = C.ckpt_options_default(n_slots=a.n_slots, bucket_bytes=a.bucket, stripe_unit=a.unit, flags=flags,
-                                  max_ctas=a.max_ctas)
+                                  max_ctas=a.max_ctas, host_buffers=host_buffers)
     ctx = C.ckpt_create(local, opts)
     t_setup = time.perf_counter()
     C.ckpt_register(ctx, descriptors(ts, specs), {"rank": rank, "world": world, "local_rank": local,
@@ -319,25 +329,6 @@ def main():
     launches = int(allsum(st["pack_launches"] + st["xor_launches"]))
 
     # co-running bf16 GEMM (the O_in-mem analog, P.234; HAS layer 2, P.423)
-    corun = None
-    if not a.no_corun:
-        corun = {"this_config": gemm_corun(torch, C, ctx, stream, a.bucket, barrier, allmax, dev)}
-        if a.pack != "ce" and not a.device_only:
-            # the zero-SM configuration a training job would use while GEMMs run: copy-engine
-            # pack (+ copy-engine gather of the peer units when protected)
-            o2 = C.ckpt_options_default(n_slots=a.n_slots, bucket_bytes=a.bucket, stripe_unit=a.unit,
-                                        flags=C.CKPT_OPT_TIMING | C.CKPT_OPT_CE_PACK
-                                        | (C.CKPT_OPT_CE_GATHER if world > 1 else 0))
-            ctx2 = C.ckpt_create(local, o2)
-            C.ckpt_register(ctx2, descriptors(ts, specs))
-            if world > 1:
-                C.protect_ipc(ctx2)
-            else:
-                C.ckpt_protect(ctx2, 1, 0)
-            corun["ce_pack"] = gemm_corun(torch, C, ctx2, stream, a.bucket, barrier, allmax, dev)
-            C.ckpt_destroy(ctx2)
-        corun["slowdown_pct"] = min(v["slowdown_pct"] for v in corun.values())
-
     # e2e through the public API: load (H2D of the completed image into the tensors)
     # + snapshot + commit (D2H), host wall clock, max over ranks
     e2e = None
@@ -359,6 +350,29 @@ def main():
                "what": "ckpt_load (restore from the completed host image) + ckpt_snapshot + ckpt_wait per step, "
                        "host wall clock, max over ranks"}
 
+    corun = None
+    if not a.no_corun:
+        corun = {"this_config": gemm_corun(torch, C, ctx, stream, a.bucket, barrier, allmax, dev)}
+    C.ckpt_destroy(ctx)  # one context (and one pinned arena) alive at a time
+    ctx = None
+    if not a.no_corun and a.pack != "ce" and not a.device_only:
+        # the zero-SM configuration a training job would use while GEMMs run: copy-engine
+        # pack (+ copy-engine gather of the peer units when protected)
+        o2 = C.ckpt_options_default(n_slots=a.n_slots, bucket_bytes=a.bucket, stripe_unit=a.unit,
+                                    host_buffers=host_buffers,
+                                    flags=C.CKPT_OPT_TIMING | C.CKPT_OPT_CE_PACK
+                                    | (C.CKPT_OPT_CE_GATHER if world > 1 else 0))
+        ctx2 = C.ckpt_create(local, o2)
+        C.ckpt_register(ctx2, descriptors(ts, specs))
+        if world > 1:
+            C.protect_ipc(ctx2)
+        else:
+            C.ckpt_protect(ctx2, 1, 0)
+        corun["ce_pack"] = gemm_corun(torch, C, ctx2, stream, a.bucket, barrier, allmax, dev)
+        C.ckpt_destroy(ctx2)
+    if corun:
+        corun["slowdown_pct"] = min(v["slowdown_pct"] for v in corun.values())
+
     cpu = None
     if rank == 0 and world == 1 and not a.no_cpu_baseline:
         gbs, desc, _, _ = oracle_sample(a.config, 1, a.cpu_seconds)
@@ -372,7 +386,7 @@ def main():
             "config": {"workload": a.config, "state_bytes_per_gpu": S, "tensors_per_gpu": len(specs),
                        "m": m, "L_star": g["L_star"], "stripe_unit": g["unit"], "bucket_bytes": a.bucket,
                        "n_slots": a.n_slots, "pack": a.pack, "gather": a.gather, "device_only": a.device_only,
-                       "max_ctas": a.max_ctas or "2 x SMs",
+                       "max_ctas": a.max_ctas or "2 x SMs", "host_buffers": host_buffers,
                        "l2": f"inputs {S / 1e9:.2f} GB/GPU >> 126 MB L2; no flush needed"},
             "per_gpu_gbs": round(value / N, 3),
             "host_link": None if a.device_only else {
@@ -385,7 +399,6 @@ def main():
             "setup_s_rank0": round(t_setup, 2),
         }
         print(json.dumps(line), flush=True)
-    C.ckpt_destroy(ctx)
     if world > 1:
         dist.destroy_process_group()
     return 0
