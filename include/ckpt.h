@@ -149,6 +149,8 @@ typedef struct ckpt_stats {      /* cumulative since ckpt_stats_reset           
     uint64_t xor_bytes_out;      /* parity bytes written                                 */
     uint64_t d2h_bytes, h2d_bytes;
     uint64_t ce_copies;          /* copy-engine operations issued (pack/gather/D2H/H2D)  */
+    uint64_t rebuild_bytes_in;   /* algorithmic: peer + parity bytes read by rebuild rows */
+    uint64_t rebuild_bytes_out;  /* rebuilt bytes stored into the lost rank (NVLink)      */
     double   pack_ms, xor_ms, unpack_ms, rebuild_ms; /* summed launch durations
                                     (only with CKPT_OPT_TIMING)                          */
     double   last_snapshot_ms;   /* capture event -> last D2H event of the last snapshot

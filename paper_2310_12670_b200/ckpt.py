@@ -73,7 +73,8 @@ class ckpt_group(ctypes.Structure):
 class ckpt_stats(ctypes.Structure):
     _fields_ = [(n, _u64) for n in ("snapshots", "loads", "rebuilds", "pack_launches", "xor_launches",
                                     "unpack_launches", "rebuild_launches", "pack_bytes", "xor_bytes_in",
-                                    "xor_bytes_out", "d2h_bytes", "h2d_bytes", "ce_copies")] + \
+                                    "xor_bytes_out", "d2h_bytes", "h2d_bytes", "ce_copies", "rebuild_bytes_in",
+                                    "rebuild_bytes_out")] + \
                [(n, ctypes.c_double) for n in ("pack_ms", "xor_ms", "unpack_ms", "rebuild_ms", "last_snapshot_ms")]
 
     def as_dict(self):

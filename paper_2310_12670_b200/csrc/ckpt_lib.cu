@@ -994,6 +994,9 @@ static int do_rebuild_row(ckpt_ctx *c, uint64_t k, uint32_t kl, cudaStream_t s) 
     rc = timed_end(t, s);
     if (rc) return rc;
     c->st.rebuild_launches++;
+    const uint64_t unit_bytes = (be - bb) / (c->m - 1);  // one unit per stripe per term
+    c->st.rebuild_bytes_in += (uint64_t)a.nin * unit_bytes;
+    c->st.rebuild_bytes_out += unit_bytes;
     return CKPT_OK;
 }
 

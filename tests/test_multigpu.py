@@ -149,7 +149,7 @@ def test_ipc_c1_16mib_all_gpus():
     _run(min(_world(), 8), ("c1_16mb_fp32_m8", 65536, 0, 64 << 20, 0, 0))
 
 
-def _worker_c2(rank, world, port, q):
+def _worker_c2(rank, world, port, q, config="c2_7b_tp8"):
     try:
         os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank), WORLD_SIZE=str(world))
         import torch
@@ -164,8 +164,8 @@ def _worker_c2(rank, world, port, q):
         torch.cuda.set_device(rank)
         dev = torch.device("cuda", rank)
         dist.init_process_group("nccl", device_id=dev)
-        specs, ts = make_rank_state("c2_7b_tp8", rank, dev)
-        ctx = C.ckpt_create(rank, C.ckpt_options_default(n_slots=0, bucket_bytes=1 << 30))  # bench defaults
+        specs, ts = make_rank_state(config, rank, dev)
+        ctx = C.ckpt_create(rank, C.ckpt_options_default(n_slots=0, bucket_bytes=512 << 20))  # bench defaults
         C.ckpt_register(ctx, descriptors(ts, specs))
         C.protect_ipc(ctx)
         g = C.ckpt_geometry(ctx)
@@ -177,7 +177,7 @@ def _worker_c2(rank, world, port, q):
         nst = g["L_star"] // stripe
         rng = np.random.default_rng(rank)
         ok = []
-        all_specs = [synth.config_tensors("c2_7b_tp8", j) for j in range(m)]
+        all_specs = [synth.config_tensors(config, j) for j in range(m)]
         for s in [0, nst - 1] + rng.integers(0, nst, 6).tolist():
             imgs = [image_slice(all_specs[j], j, s * stripe, stripe) for j in range(m)]
             want = oracle.encode(imgs, u, rank)
@@ -192,10 +192,11 @@ def _worker_c2(rank, world, port, q):
         q.put((rank, None, traceback.format_exc()))
 
 
-def test_ipc_c2_7b_full_size_sampled():
-    """BASELINE config 2 at full size in the bench launch configuration (one process per
-    GPU, full-copy staging, 1 GiB buckets): sampled stripes of data and parity of every
-    rank against the oracle."""
+@pytest.mark.parametrize("config", ["c2_7b_tp8", "c4_34b_tp8_stage0"])
+def test_ipc_full_size_sampled(config):
+    """BASELINE configs 2 and 4 at full size in the bench launch configuration (one
+    process per GPU, full-copy staging, 512 MiB buckets): sampled stripes of data and
+    parity of every rank against the oracle."""
     world = min(_world(), 8)
     import queue
     import time
@@ -204,7 +205,7 @@ def test_ipc_c2_7b_full_size_sampled():
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    ps = [ctx.Process(target=_worker_c2, args=(r, world, port, q)) for r in range(world)]
+    ps = [ctx.Process(target=_worker_c2, args=(r, world, port, q, config)) for r in range(world)]
     for p in ps:
         p.start()
     res, t0 = [], time.time()

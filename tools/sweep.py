@@ -95,6 +95,7 @@ def main():
                "launches_per_snapshot": (st["pack_launches"] + st["xor_launches"]) // a.reps}
         if a.drill and g["m"] >= 2:
             lost = [int(x) for x in a.lost.split(",")] if a.lost else [0, g["m"] - 1]
+            C.ckpt_stats_reset(ctx)
             for k in lost:
                 fill_state(ts, rank, seed=999 + k, xor_mode=1)  # later steps mutate everything
                 if rank == k:
@@ -110,6 +111,7 @@ def main():
                 torch.cuda.synchronize()
                 t2 = time.perf_counter()
                 rb, ld = amax(t1 - t0), amax(t2 - t1)
+                srb = C.ckpt_get_stats(ctx)
                 # bit-exact: every tensor of every rank equals the generator (sampled bytes)
                 ok = True
                 from synth import SEED, fill as gfill
@@ -118,8 +120,14 @@ def main():
                     got = ts[ti].view(torch.uint8)[:n].cpu().numpy()
                     ok = ok and bool((got == gfill(SEED, rank, ti, n)).all())
                 okall = amax(0.0 if ok else 1.0) == 0.0
+                # rebuild kernel of this rank (a row owner), per launch: NVLink/HBM bytes in +
+                # bytes stored into the lost rank over NVLink, / mean launch time
+                kgbs = (srb["rebuild_bytes_in"] + srb["rebuild_bytes_out"]) / max(srb["rebuild_ms"], 1e-9) / 1e6
                 rec.setdefault("drill", []).append({"lost": k, "rebuild_ms": round(rb * 1e3, 2), "load_ms": round(ld * 1e3, 2),
-                                                    "bit_exact_sampled": okall})
+                                                    "bit_exact_sampled": okall,
+                                                    "rank0_rebuild_kernel_gbs": round(kgbs, 1) if rank != k else None,
+                                                    "rank0_rebuild_launches": srb["rebuild_launches"]})
+                C.ckpt_stats_reset(ctx)
         if rank == 0:
             print(json.dumps(rec), flush=True)
         C.ckpt_destroy(ctx)
