@@ -53,10 +53,14 @@ def lib():
         L.oracle_encode.argtypes = [_u64, _p, _u64, _u64, _u64, _p]
         L.oracle_rebuild.argtypes = [_u64, _p, _p, _u64, _u64, _u64, _p, _p]
         L.oracle_fill.argtypes = [_u64, _u64, _u64, _u64, _u64, _p]
+        L.oracle_arc_holder.argtypes = [_u64, _u64]
+        L.oracle_arc_holder.restype = _u64
+        L.oracle_arc_copy.argtypes = [_u64, _p, _u64, _u64, _p]
+        L.oracle_recover.argtypes = [_u64, _u64, _p, _p, _p, _p, _p, _u64, _u64, _p, _p]
         L.oracle_splitmix64.argtypes = [_u64]
         L.oracle_splitmix64.restype = _u64
         for f in ("oracle_layout", "oracle_common_length", "oracle_pack", "oracle_unpack",
-                  "oracle_encode", "oracle_rebuild", "oracle_fill"):
+                  "oracle_encode", "oracle_rebuild", "oracle_fill", "oracle_arc_copy", "oracle_recover"):
             getattr(L, f).restype = ctypes.c_int
         _lib = L
     return _lib
@@ -159,6 +163,47 @@ def rebuild(Ds, Ps, u: int, k: int, lost=None) -> np.ndarray:
                               lost_arr.ctypes.data if lost_arr is not None else None,
                               Dk.ctypes.data), "rebuild")
     return Dk
+
+
+# ---- ARC / collaborative protection -----------------------------
+SCHEME_AEC, SCHEME_ARC, SCHEME_ARC_AEC = 1, 2, 3
+
+
+def arc_holder(m: int, x: int) -> int:
+    """Member holding the ARC copy of member x (ring placement, SPEC S.313)."""
+    return int(lib().oracle_arc_holder(m, x))
+
+
+def arc_copy(Ds, i: int) -> np.ndarray:
+    """ARC copy held by member i: the image of member (i+1) mod m."""
+    Ds = [np.ascontiguousarray(d, dtype=np.uint8) for d in Ds]
+    out = np.empty(Ds[0].size, dtype=np.uint8)
+    ptr = _ptrs(Ds)
+    _chk(lib().oracle_arc_copy(len(Ds), ptr.ctypes.data, Ds[0].size, i, out.ctypes.data), "arc_copy")
+    return out
+
+
+def recover(scheme: int, lost, Ds, Ps, MDs, MPs, u: int):
+    """REFT-load step 3 for up to two losses; returns {x: (D_x, P_x or None)}.
+    Entries of lost members in Ds/Ps/MDs/MPs may be None (never read)."""
+    m = len(Ds)
+    sizes = [d.size for d in list(Ds) + list(MDs or []) if d is not None]
+    if not sizes:
+        raise OracleError("recover: unrecoverable (no surviving member)")
+    Lstar = sizes[0]
+    pb = Lstar // max(m - 1, 1)
+    aec = scheme in (SCHEME_AEC, SCHEME_ARC_AEC)
+    lost_arr = np.array([1 if x else 0 for x in lost], dtype=np.uint8)
+    outD = [np.zeros(Lstar, np.uint8) if lost[j] else None for j in range(m)]
+    outP = [np.zeros(pb, np.uint8) if lost[j] and aec else None for j in range(m)]
+    keep = [[np.ascontiguousarray(a, dtype=np.uint8) if a is not None else None for a in arr]
+            for arr in (Ds, Ps or [None] * m, MDs or [None] * m, MPs or [None] * m)]
+    ptrs = [_ptrs(k) for k in keep]
+    po, pp = _ptrs(outD), _ptrs(outP)
+    _chk(lib().oracle_recover(m, scheme, lost_arr.ctypes.data, ptrs[0].ctypes.data, ptrs[1].ctypes.data,
+                              ptrs[2].ctypes.data, ptrs[3].ctypes.data, Lstar, u, po.ctypes.data, pp.ctypes.data),
+         "recover")
+    return {j: (outD[j], outP[j]) for j in range(m) if lost[j]}
 
 
 # ---- generator (oracle's own copy; not part of the method) ------------------------

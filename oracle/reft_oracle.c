@@ -185,3 +185,76 @@ int oracle_fill(uint64_t seed, uint64_t j, uint64_t t, uint64_t byte_begin,
     }
     return ORACLE_OK;
 }
+
+/* ---- ARC and collaborative protection --------------------
+ * ARC, "Asynchronous Redundant Copying" (P.456-460): "each member not only saves its own
+ * shard to a snapshot but also saves shards from peer members", doubling the volume to
+ * 2 W_n/m; placement is the ring of SPEC S.313: member i also holds member (i+1) mod m's
+ * image.  Collaborative protection (P.507-508): with ARC and AEC both enabled, "N or
+ * fewer node failures" per group (N = 2) are restored.  Reading Q20: the
+ * ARC copy in ARC+AEC holds the neighbour's parity row as well as its data, which is
+ * what makes every pair of losses recoverable for m >= 3 (an adjacent pair a, a+1
+ * would otherwise lose the parity row of a, which covers one unit of every stripe of
+ * a+1). */
+
+/* Member holding the ARC copy of member x's image: (x - 1) mod m. */
+uint64_t oracle_arc_holder(uint64_t m, uint64_t x) { return (x + m - 1) % m; }
+
+/* ARC copy held by member i: the image of member (i+1) mod m, byte for byte. */
+int oracle_arc_copy(uint64_t m, const uint8_t *const *D, uint64_t Lstar, uint64_t i, uint8_t *out)
+{
+    uint64_t b, src;
+    if (m < 2 || i >= m || !D || (!out && Lstar)) return ORACLE_EINVAL;
+    src = (i + 1) % m;
+    for (b = 0; b < Lstar; b++) out[b] = D[src][b];
+    return ORACLE_OK;
+}
+
+/* REFT-load step 3 (P.545) for up to two losses.  scheme: 1 = AEC, 2 = ARC, 3 = ARC+AEC.
+ * Inputs per member j: D[j] data image (L* bytes), P[j] parity row (L* /(m-1) bytes,
+ * AEC schemes), MD[j] / MP[j] the ARC copy of member j+1's data / parity held by j.
+ * Entries of lost members are never read.  lost[j] != 0 marks the losses.
+ * Outputs, for every lost x: outD[x] (and outP[x] for AEC schemes).
+ *   1. every lost x whose holder h = x-1 survived takes D_x = MD[h] (and P_x = MP[h]);
+ *   2. if exactly one loss x remains and the scheme has AEC, D_x follows O6 from the
+ *      other members' data and parity (restored ones included) and P_x follows O4;
+ *   3. anything else is unrecoverable. */
+int oracle_recover(uint64_t m, uint64_t scheme, const uint8_t *lost, const uint8_t *const *D,
+                   const uint8_t *const *P, const uint8_t *const *MD, const uint8_t *const *MP,
+                   uint64_t Lstar, uint64_t u, uint8_t *const *outD, uint8_t *const *outP)
+{
+    uint64_t j, b, nlost = 0, pbytes, left = 0, x = 0;
+    int arc = scheme == 2 || scheme == 3, aec = scheme == 1 || scheme == 3;
+    const uint8_t *Dv[8], *Pv[8];
+    uint8_t restored[8] = {0};
+    if (m < 2 || m > 8 || !lost || !D || !outD || (!arc && !aec)) return m < 2 ? ORACLE_EUNRECOVERABLE : ORACLE_EINVAL;
+    if (aec && (u == 0 || Lstar % ((m - 1) * u))) return ORACLE_EINVAL;
+    pbytes = Lstar / (m - 1);
+    for (j = 0; j < m; j++) nlost += lost[j] ? 1 : 0;
+    if (nlost > 2) return ORACLE_EUNRECOVERABLE;
+    for (j = 0; j < m; j++) {
+        Dv[j] = lost[j] ? 0 : D[j];
+        Pv[j] = (lost[j] || !aec) ? 0 : P[j];
+    }
+    if (arc) {                                   /* step 1 */
+        for (j = 0; j < m; j++) {
+            uint64_t h = oracle_arc_holder(m, j);
+            if (!lost[j] || lost[h]) continue;
+            for (b = 0; b < Lstar; b++) outD[j][b] = MD[h][b];
+            if (aec) for (b = 0; b < pbytes; b++) outP[j][b] = MP[h][b];
+            Dv[j] = outD[j];
+            if (aec) Pv[j] = outP[j];
+            restored[j] = 1;
+        }
+    }
+    for (j = 0; j < m; j++)
+        if (lost[j] && !restored[j]) { left++; x = j; }
+    if (left == 0) return ORACLE_OK;
+    if (left > 1 || !aec) return ORACLE_EUNRECOVERABLE;
+    {                                            /* step 2 */
+        int rc = oracle_rebuild(m, Dv, Pv, Lstar, u, x, 0, outD[x]);
+        if (rc) return rc;
+        Dv[x] = outD[x];
+        return oracle_encode(m, Dv, Lstar, u, x, outP[x]);
+    }
+}

@@ -226,3 +226,90 @@ def test_two_losses_unrecoverable():
                        [True, True, False, False])
     with pytest.raises(oracle.OracleError, match="unrecoverable"):
         oracle.rebuild([Ds[0]], [Ps[0]], 1, 0)
+
+
+# ---------------------------------------------------------------- ARC / collaborative (f2)
+def test_arc_ring_placement_and_volume():
+    # S.313-318: node i also snapshots node (i+1) mod m; the copies cover every shard
+    # exactly once; per-node volume 2 W_n/m (W_n=1000, m=4 -> 500); m=2 -> each holds W_n
+    for m in range(2, 9):
+        held = sorted((i + 1) % m for i in range(m))
+        assert held == list(range(m))
+        assert all(oracle.arc_holder(m, (i + 1) % m) == i for i in range(m))
+    W_n, m = 1000, 4
+    Ds = rand_images(m, W_n // m, 3)
+    for i in range(m):
+        copy = oracle.arc_copy(Ds, i)
+        assert np.array_equal(copy, Ds[(i + 1) % m])
+        assert Ds[i].size + copy.size == 2 * W_n // m == 500
+    D2 = rand_images(2, 500, 4)
+    assert D2[0].size + oracle.arc_copy(D2, 0).size == 1000
+
+
+def _group(m, u, seed):
+    Lstar = (m - 1) * u * 3
+    Ds = rand_images(m, Lstar, seed)
+    Ps = oracle.encode_all(Ds, u)
+    MDs = [oracle.arc_copy(Ds, i) for i in range(m)]
+    MPs = [Ps[(i + 1) % m] for i in range(m)]  # ARC+AEC: the neighbour's parity row too (Q20)
+    return Ds, Ps, MDs, MPs
+
+
+def _lose(arrs, lost):
+    return [[None if lost[j] else a for j, a in enumerate(arr)] for arr in arrs]
+
+
+@pytest.mark.parametrize("m", [3, 4, 5, 6])
+def test_collaborative_tolerates_every_pair(m):
+    # P.507-508 / S.364-366: ARC + AEC together restore any N = 2 failures (m >= 3),
+    # bit-exactly (data and parity rows) -- brute force over every pair
+    u = 2
+    Ds, Ps, MDs, MPs = _group(m, u, 50 + m)
+    for a, b in itertools.combinations(range(m), 2):
+        lost = [j in (a, b) for j in range(m)]
+        out = oracle.recover(oracle.SCHEME_ARC_AEC, lost, *_lose((Ds, Ps, MDs, MPs), lost), u)
+        for x in (a, b):
+            assert np.array_equal(out[x][0], Ds[x]) and np.array_equal(out[x][1], Ps[x]), (a, b, x)
+
+
+@pytest.mark.parametrize("m", [2, 3, 4, 6])
+def test_single_strategy_tolerates_one(m):
+    # S.364-365: ARC alone and AEC alone restore any single failure; each fails on some
+    # pair (AEC on every pair, ARC on an adjacent pair); three losses are never restored
+    u = 4
+    Ds, Ps, MDs, MPs = _group(m, u, 90 + m)
+    for x in range(m):
+        lost = [j == x for j in range(m)]
+        for scheme in (oracle.SCHEME_ARC, oracle.SCHEME_AEC, oracle.SCHEME_ARC_AEC):
+            out = oracle.recover(scheme, lost, *_lose((Ds, Ps, MDs, MPs), lost), u)
+            assert np.array_equal(out[x][0], Ds[x])
+    lost = [j in (0, 1) for j in range(m)]
+    for scheme in (oracle.SCHEME_ARC, oracle.SCHEME_AEC):
+        with pytest.raises(oracle.OracleError, match="unrecoverable"):
+            oracle.recover(scheme, lost, *_lose((Ds, Ps, MDs, MPs), lost), u)
+    if m >= 4:  # ARC alone does restore a non-adjacent pair
+        lost = [j in (0, 2) for j in range(m)]
+        out = oracle.recover(oracle.SCHEME_ARC, lost, *_lose((Ds, Ps, MDs, MPs), lost), u)
+        assert np.array_equal(out[0][0], Ds[0]) and np.array_equal(out[2][0], Ds[2])
+    if m >= 3:
+        lost = [j in (0, 1, 2) for j in range(m)]
+        with pytest.raises(oracle.OracleError, match="unrecoverable"):
+            oracle.recover(oracle.SCHEME_ARC_AEC, lost, *_lose((Ds, Ps, MDs, MPs), lost), u)
+
+
+def test_collaborative_needs_mirrored_parity():
+    # why reading Q20 mirrors the parity row: without it an adjacent pair (a, a+1) leaves
+    # unit sigma(a, a+1) of every stripe of a+1 uncovered -- show that unit is exactly
+    # the one the other rows cannot provide
+    m, u = 4, 1
+    Ds, Ps, MDs, MPs = _group(m, u, 7)
+    lost = [True, True, False, False]
+    out = oracle.recover(oracle.SCHEME_ARC_AEC, lost, *_lose((Ds, Ps, MDs, MPs), lost), u)
+    assert np.array_equal(out[1][0], Ds[1])
+    bad_MPs = [None, None, MPs[2], np.zeros_like(MPs[3])]  # member 3 holds member 0's parity: zeroed
+    out = oracle.recover(oracle.SCHEME_ARC_AEC, lost, Ds[:0] + [None, None, Ds[2], Ds[3]],
+                         [None, None, Ps[2], Ps[3]], [None, None, MDs[2], MDs[3]], bad_MPs, u)
+    diff = np.nonzero(out[1][0] != Ds[1])[0]
+    stripe = (m - 1) * u
+    # only bytes of unit sigma(0, 1) = 0 of each stripe of member 1 are wrong
+    assert diff.size and all(d % stripe < u for d in diff)
