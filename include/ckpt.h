@@ -72,6 +72,9 @@ extern "C" {
                                       D2H, no host arena; load/rebuild work from HBM.  A
                                       single device image: a failed snapshot destroys the
                                       previous one.  Measures the device-side protect path. */
+#define CKPT_OPT_SHM_ARENA   0x40u /* host arena in POSIX shared memory (/dev/shm), one file
+                                      per member and host buffer: peers (ARC) and a restarted
+                                      process can reach it; required by the ARC schemes     */
 
 typedef struct ckpt_options {
     uint32_t struct_size;   /* sizeof(ckpt_options); set by ckpt_options_default       */
@@ -131,11 +134,22 @@ typedef struct ckpt_layout {   /* the hybrid-parallel position of this rank (P.3
 
 typedef struct ckpt_ctx ckpt_ctx;
 
+/* Protection schemes (P.349, P.435-508).  AEC: rotated XOR parity, one parity row per
+ * member (tolerates 1 loss).  ARC: member i's host arena also holds a copy of member
+ * (i+1) mod m's image (ring placement, SPEC S.313; volume 2 W_n/m, P.459; tolerates 1
+ * loss).  ARC_AEC: both, with the ARC copy carrying the neighbour's parity row too
+ * (reading Q20) -- "collaborative protection" tolerating any 2 losses for m >= 3 (P.507). */
+#define CKPT_SCHEME_DEFAULT  0u   /* = AEC                                               */
+#define CKPT_SCHEME_AEC      1u
+#define CKPT_SCHEME_ARC      2u
+#define CKPT_SCHEME_ARC_AEC  3u
+
 typedef struct ckpt_group {
     uint32_t         m;          /* group size, 1 <= m <= CKPT_MAX_GROUP                 */
     uint32_t         my_index;   /* this context's member index in [0, m)               */
     uint32_t         transport;  /* CKPT_GROUP_IPC or CKPT_GROUP_LOCAL                  */
-    uint32_t         reserved;
+    uint32_t         scheme;     /* CKPT_SCHEME_*; ARC schemes need CKPT_OPT_SHM_ARENA
+                                    and full-copy staging (n_slots = 0)                  */
     const void      *handles;    /* IPC: m * CKPT_HANDLE_BYTES blobs from
                                     ckpt_export_handle, in member order                 */
     ckpt_ctx *const *members;    /* LOCAL: the m contexts, in member order              */
@@ -242,13 +256,26 @@ int ckpt_load(ckpt_ctx *ctx, void *stream);
  * one loss), EINVAL, ENOSNAP, ECUDA. */
 int ckpt_rebuild(ckpt_ctx *ctx, int32_t lost_rank, void *stream);
 
+/* REFT-load step 3 for up to two losses (P.545; collaborative protection P.507-508).
+ * COLLECTIVE and host-blocking; every member passes the same lost_mask (bit j = member
+ * j lost both its tensors and its host image).  Order (the oracle's oracle_recover):
+ * (1) every lost member x whose ARC holder x-1 survived takes its completed image (and
+ * parity row) from the holder's ARC copy; (2) a single remaining loss is rebuilt from
+ * parity as in ckpt_rebuild; (3) the ARC copies held by lost members are re-created from
+ * their neighbours' completed images.  Follow with ckpt_load on every member.
+ * Errors: EUNRECOVERABLE (the losses exceed what the scheme restores), EINVAL, ENOSNAP,
+ * ECUDA, EPEER. */
+int ckpt_recover(ckpt_ctx *ctx, uint32_t lost_mask, void *stream);
+
 /* Failure injection for drills (Q12, hardware-loss semantics): overwrite this
  * member's completed and ongoing host images with `poison` and mark it as having no
  * completed snapshot (it can only be restored by ckpt_rebuild). */
 int ckpt_forget(ckpt_ctx *ctx, uint8_t poison);
 
 /* Read-only view of the completed (which = 0) or ongoing (which = 1) host image:
- * data (L* bytes) and parity (L* /(m-1) bytes, NULL/0 when unprotected).
+ * data (L* bytes) and parity (L* /(m-1) bytes, NULL/0 when unprotected).  which = 2 / 3:
+ * the ARC copy (completed / ongoing) this member holds of member (i+1) mod m: data and,
+ * for ARC_AEC, that member's parity row.
  * Errors: EINVAL, ENOSNAP (which = 0 and nothing committed). */
 int ckpt_host_view(const ckpt_ctx *ctx, int which, const void **data, uint64_t *dlen,
                    const void **parity, uint64_t *plen);

@@ -35,6 +35,8 @@ CKPT_OPT_LSU_PACK = 0x4
 CKPT_OPT_CE_PACK = 0x8
 CKPT_OPT_CE_GATHER = 0x10
 CKPT_OPT_DEVICE_ONLY = 0x20
+CKPT_OPT_SHM_ARENA = 0x40
+CKPT_SCHEME_DEFAULT, CKPT_SCHEME_AEC, CKPT_SCHEME_ARC, CKPT_SCHEME_ARC_AEC = 0, 1, 2, 3
 
 CKPT_DTYPE_BYTES, CKPT_DTYPE_BF16, CKPT_DTYPE_FP16, CKPT_DTYPE_FP32 = 0, 1, 2, 3
 CKPT_ROLE_PARAM, CKPT_ROLE_MASTER, CKPT_ROLE_EXP_AVG, CKPT_ROLE_EXP_AVG_SQ, CKPT_ROLE_OTHER = 0, 1, 2, 3, 4
@@ -66,7 +68,7 @@ class ckpt_layout(ctypes.Structure):
 
 
 class ckpt_group(ctypes.Structure):
-    _fields_ = [("m", _u32), ("my_index", _u32), ("transport", _u32), ("reserved", _u32),
+    _fields_ = [("m", _u32), ("my_index", _u32), ("transport", _u32), ("scheme", _u32),
                 ("handles", _vp), ("members", ctypes.POINTER(_vp))]
 
 
@@ -113,6 +115,7 @@ def lib():
             "ckpt_wait": (ctypes.c_int, [_vp, _u64]),
             "ckpt_load": (ctypes.c_int, [_vp, _vp]),
             "ckpt_rebuild": (ctypes.c_int, [_vp, _i32, _vp]),
+            "ckpt_recover": (ctypes.c_int, [_vp, _u32, _vp]),
             "ckpt_forget": (ctypes.c_int, [_vp, ctypes.c_uint8]),
             "ckpt_host_view": (ctypes.c_int, [_vp, ctypes.c_int, ctypes.POINTER(_vp), ctypes.POINTER(_u64),
                                               ctypes.POINTER(_vp), ctypes.POINTER(_u64)]),
@@ -224,9 +227,10 @@ def ckpt_export_handle(ctx: int) -> bytes:
 
 
 def ckpt_protect(ctx: int, m: int, my_index: int, transport: int = CKPT_GROUP_IPC,
-                 handles: Optional[bytes] = None, members: Optional[Sequence[int]] = None) -> int:
+                 handles: Optional[bytes] = None, members: Optional[Sequence[int]] = None,
+                 scheme: int = CKPT_SCHEME_DEFAULT) -> int:
     """Returns CKPT_OK, or CKPT_EUNAVAIL for m == 1 (snapshot-only; not an error)."""
-    g = ckpt_group(m, my_index, transport, 0, None, None)
+    g = ckpt_group(m, my_index, transport, scheme, None, None)
     keep = None
     if handles is not None:
         keep = ctypes.create_string_buffer(handles, len(handles))
@@ -260,6 +264,10 @@ def ckpt_load(ctx: int, stream=None) -> None:
 
 def ckpt_rebuild(ctx: int, lost_rank: int, stream=None) -> None:
     _check(lib().ckpt_rebuild(ctx, lost_rank, _stream_handle(stream)), "ckpt_rebuild")
+
+
+def ckpt_recover(ctx: int, lost_mask: int, stream=None) -> None:
+    _check(lib().ckpt_recover(ctx, lost_mask, _stream_handle(stream)), "ckpt_recover")
 
 
 def ckpt_forget(ctx: int, poison: int = 0xA5) -> None:
@@ -325,21 +333,21 @@ def exchange_handles(blob: bytes, group=None) -> bytes:
     return b"".join(bytes(o.cpu().numpy().tobytes()) for o in outs)
 
 
-def protect_ipc(ctx: int, group=None) -> int:
+def protect_ipc(ctx: int, group=None, scheme: int = CKPT_SCHEME_DEFAULT) -> int:
     """Collective: bind the torch.distributed group (one process per GPU of one node) as
     the protection group; member index = rank in ``group``."""
     import torch.distributed as dist
     blobs = exchange_handles(ckpt_export_handle(ctx), group)
     m, me = dist.get_world_size(group), dist.get_rank(group)
-    rc = ckpt_protect(ctx, m, me, CKPT_GROUP_IPC, handles=blobs)
+    rc = ckpt_protect(ctx, m, me, CKPT_GROUP_IPC, handles=blobs, scheme=scheme)
     dist.barrier(group)
     return rc
 
 
-def protect_local(ctxs: Sequence[int]) -> None:
+def protect_local(ctxs: Sequence[int], scheme: int = CKPT_SCHEME_DEFAULT) -> None:
     """Bind m contexts of this process (same or different devices) as one group."""
     for i, c in enumerate(ctxs):
-        ckpt_protect(c, len(ctxs), i, CKPT_GROUP_LOCAL, members=list(ctxs))
+        ckpt_protect(c, len(ctxs), i, CKPT_GROUP_LOCAL, members=list(ctxs), scheme=scheme)
 
 
 # ---------------------------------------------------------------- harness generator

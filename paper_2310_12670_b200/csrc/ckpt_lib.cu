@@ -29,8 +29,12 @@
 #include <thread>
 #include <vector>
 
+#include <fcntl.h>
 #include <sys/mman.h>
+#include <sys/stat.h>
 #include <unistd.h>
+
+#include <random>
 
 #include "../../include/ckpt.h"
 #include "ckpt_kernels.cuh"
@@ -104,6 +108,7 @@ struct HandleBlob {  // exported by ckpt_export_handle; fixed layout, <= CKPT_HA
     uint32_t n_slots;       // 0 = full copy
     uint32_t full_copy;
     uint64_t staging_bytes;
+    uint64_t nonce;         // random per context; member 0's names the group's shm arena
     char host[64];
     cudaIpcMemHandle_t staging_h;
     cudaIpcMemHandle_t flags_h;
@@ -124,10 +129,13 @@ struct TimedLaunch {
     int kind;  // 0 pack 1 xor 2 unpack 3 rebuild
 };
 
+enum HostKind { kNone = 0, kCudaHost = 1, kAnon = 2, kShmOwn = 3, kShmPeer = 4, kView = 5 };
 struct HostBuf {
     uint8_t *p = nullptr;
     uint64_t bytes = 0;
-    bool mmapped = false;
+    int kind = kNone;
+    bool registered = false;
+    std::string name;  // shm object name (kShmOwn: unlinked at free)
 };
 }  // namespace
 
@@ -177,6 +185,14 @@ struct ckpt_ctx {
 
     // host arena
     HostBuf hdata[2], hpar[2];
+    // protection scheme and the shared-memory arena (CKPT_OPT_SHM_ARENA): one file per
+    // member and host buffer, [data L*][parity P][ARC copy data L*][ARC copy parity P]
+    uint32_t scheme = CKPT_SCHEME_AEC;
+    bool arc = false, aec = true;
+    uint64_t my_nonce = 0, group_nonce = 0;
+    HostBuf shm_own[2], shm_hold[2], shm_next[2];  // mine, my ARC holder's, member me+1's
+    uint8_t *harc[2] = {}, *harcp[2] = {};          // the ARC copy I hold (of member me+1)
+    bool arc_dirty[2] = {false, false};             // its zero pad was poisoned
     int nbuf = 2;
     int completed = -1, ongoing = 0;
     bool pad_dirty[2] = {false, false};  // zero pad [L, L*) overwritten by ckpt_forget
@@ -201,6 +217,9 @@ struct ckpt_ctx {
     uint32_t op_seq_base = 0;
     bool rebuild_requested = false;
     int32_t rebuild_lost = -1;
+    bool recover_requested = false;
+    uint32_t recover_mask = 0;
+    void *recover_stream = nullptr;
 
     // stats
     ckpt_stats st{};
@@ -269,6 +288,31 @@ static int harvest_timing(ckpt_ctx *c) {
 // Pinned host memory: anonymous mmap with transparent huge pages, pre-faulted by a few
 // threads, then cudaHostRegister (page-locked, device-mapped).  Falls back to
 // cudaHostAlloc.  Zero-filled (the pad of the image must read as zero, Q5).
+static void prefault(uint8_t *p, uint64_t len) {
+    unsigned nt = std::min(16u, std::max(1u, std::thread::hardware_concurrency() / 2));
+    std::vector<std::thread> th;
+    const uint64_t per = align_up(len / nt + 1, 2ull << 20);
+    for (unsigned i = 0; i < nt; ++i)
+        th.emplace_back([=] {
+            for (uint64_t o = i * per; o < std::min(len, (i + 1) * per); o += 4096) p[o] = 0;
+        });
+    for (auto &t : th) t.join();
+}
+
+// Host copies of whole images (ARC restore): a few threads, large pieces.
+static void parallel_memcpy(uint8_t *dst, const uint8_t *src, uint64_t n) {
+    unsigned nt = std::min(16u, std::max(1u, std::thread::hardware_concurrency() / 2));
+    if (n < (64ull << 20)) nt = 1;
+    std::vector<std::thread> th;
+    const uint64_t per = align_up(n / nt + 1, 4096);
+    for (unsigned i = 0; i < nt; ++i)
+        th.emplace_back([=] {
+            const uint64_t lo = i * per, hi = std::min(n, (i + 1) * per);
+            if (lo < hi) memcpy(dst + lo, src + lo, hi - lo);
+        });
+    for (auto &t : th) t.join();
+}
+
 static int host_alloc(HostBuf &b, uint64_t bytes) {
     b = HostBuf{};
     if (bytes == 0) return CKPT_OK;
@@ -278,19 +322,12 @@ static int host_alloc(HostBuf &b, uint64_t bytes) {
 #ifdef MADV_HUGEPAGE
         madvise(p, len, MADV_HUGEPAGE);
 #endif
-        unsigned nt = std::min(16u, std::max(1u, std::thread::hardware_concurrency() / 2));
-        std::vector<std::thread> th;
-        const uint64_t per = align_up(len / nt + 1, 2ull << 20);
-        for (unsigned i = 0; i < nt; ++i)
-            th.emplace_back([=] {
-                uint8_t *q = (uint8_t *)p;
-                for (uint64_t o = i * per; o < std::min(len, (i + 1) * per); o += 4096) q[o] = 0;
-            });
-        for (auto &t : th) t.join();
+        prefault((uint8_t *)p, len);
         if (cudaHostRegister(p, len, cudaHostRegisterPortable) == cudaSuccess) {
             b.p = (uint8_t *)p;
             b.bytes = len;
-            b.mmapped = true;
+            b.kind = kAnon;
+            b.registered = true;
             return CKPT_OK;
         }
         cudaGetLastError();
@@ -304,16 +341,99 @@ static int host_alloc(HostBuf &b, uint64_t bytes) {
     memset(q, 0, bytes);
     b.p = (uint8_t *)q;
     b.bytes = bytes;
+    b.kind = kCudaHost;
+    return CKPT_OK;
+}
+
+// POSIX shared memory: create (owner) or map (peer, waiting up to CKPT_TIMEOUT_S for the
+// owner to create it at full size).  Pinned with cudaHostRegister when `reg`.
+static std::string shm_name(uint64_t nonce, uint32_t member, int buf) {
+    char s[64];
+    snprintf(s, sizeof s, "/reft-%016llx-%u-%d", (unsigned long long)nonce, member, buf);
+    return s;
+}
+
+static int shm_create(HostBuf &b, const std::string &name, uint64_t bytes) {
+    b = HostBuf{};
+    const uint64_t len = align_up(std::max<uint64_t>(bytes, 1), 2ull << 20);
+    int fd = shm_open(name.c_str(), O_CREAT | O_EXCL | O_RDWR, 0600);
+    if (fd < 0) return fail(CKPT_ENOMEM, "shm_open(%s) failed: %s", name.c_str(), strerror(errno));
+    if (ftruncate(fd, (off_t)len) != 0) {
+        close(fd);
+        shm_unlink(name.c_str());
+        return fail(CKPT_ENOMEM, "ftruncate(%s, %llu) failed: %s", name.c_str(), (unsigned long long)len, strerror(errno));
+    }
+    void *p = mmap(nullptr, len, PROT_READ | PROT_WRITE, MAP_SHARED, fd, 0);
+    close(fd);
+    if (p == MAP_FAILED) {
+        shm_unlink(name.c_str());
+        return fail(CKPT_ENOMEM, "mmap(%s) failed: %s", name.c_str(), strerror(errno));
+    }
+#ifdef MADV_HUGEPAGE
+    madvise(p, len, MADV_HUGEPAGE);
+#endif
+    prefault((uint8_t *)p, len);  // allocates the tmpfs pages (zero-filled)
+    if (cudaHostRegister(p, len, cudaHostRegisterPortable) != cudaSuccess) {
+        cudaGetLastError();
+        munmap(p, len);
+        shm_unlink(name.c_str());
+        return fail(CKPT_ENOMEM, "cudaHostRegister of shm %s (%llu bytes) failed", name.c_str(), (unsigned long long)len);
+    }
+    b.p = (uint8_t *)p;
+    b.bytes = len;
+    b.kind = kShmOwn;
+    b.registered = true;
+    b.name = name;
+    return CKPT_OK;
+}
+
+static int shm_map(HostBuf &b, const std::string &name, uint64_t bytes, bool reg) {
+    b = HostBuf{};
+    const uint64_t len = align_up(std::max<uint64_t>(bytes, 1), 2ull << 20);
+    double limit = 600.0;
+    if (const char *e = getenv("CKPT_TIMEOUT_S")) limit = atof(e);
+    auto t0 = std::chrono::steady_clock::now();
+    int fd = -1;
+    for (;;) {
+        fd = shm_open(name.c_str(), O_RDWR, 0600);
+        if (fd >= 0) {
+            struct stat st;
+            if (fstat(fd, &st) == 0 && (uint64_t)st.st_size >= len) break;
+            close(fd);
+            fd = -1;
+        }
+        if (std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count() > limit)
+            return fail(CKPT_EPEER, "shm %s did not appear within %.0f s", name.c_str(), limit);
+        std::this_thread::sleep_for(std::chrono::milliseconds(2));
+    }
+    void *p = mmap(nullptr, len, PROT_READ | PROT_WRITE, MAP_SHARED, fd, 0);
+    close(fd);
+    if (p == MAP_FAILED) return fail(CKPT_EPEER, "mmap(%s) failed: %s", name.c_str(), strerror(errno));
+    if (reg && cudaHostRegister(p, len, cudaHostRegisterPortable) != cudaSuccess) {
+        cudaGetLastError();
+        munmap(p, len);
+        return fail(CKPT_EPEER, "cudaHostRegister of peer shm %s failed", name.c_str());
+    }
+    b.p = (uint8_t *)p;
+    b.bytes = len;
+    b.kind = kShmPeer;
+    b.registered = reg;
+    b.name = name;
     return CKPT_OK;
 }
 
 static void host_free(HostBuf &b) {
     if (!b.p) return;
-    if (b.mmapped) {
-        cudaHostUnregister(b.p);
-        munmap(b.p, b.bytes);
-    } else {
-        cudaFreeHost(b.p);
+    switch (b.kind) {
+        case kCudaHost: cudaFreeHost(b.p); break;
+        case kAnon:
+        case kShmOwn:
+        case kShmPeer:
+            if (b.registered) cudaHostUnregister(b.p);
+            munmap(b.p, b.bytes);
+            if (b.kind == kShmOwn) shm_unlink(b.name.c_str());
+            break;
+        default: break;  // kView: not owned
     }
     b = HostBuf{};
 }
@@ -413,6 +533,11 @@ extern "C" int ckpt_create(int device, const ckpt_options *o, ckpt_ctx **out) {
     if (device < 0 || device >= ndev) return fail(CKPT_EINVAL, "create: device %d out of range", device);
     ckpt_ctx *c = new ckpt_ctx();
     c->device = device;
+    {
+        std::random_device rd;
+        c->my_nonce = ((uint64_t)rd() << 32) ^ rd() ^ ((uint64_t)getpid() << 16) ^
+                      (uint64_t)std::chrono::steady_clock::now().time_since_epoch().count();
+    }
     c->opt = opt;
     c->nbuf = (int)opt.host_buffers;
     int rc = set_dev(c);
@@ -481,6 +606,9 @@ extern "C" int ckpt_destroy(ckpt_ctx *c) {
     for (int i = 0; i < 2; ++i) {
         host_free(c->hdata[i]);
         host_free(c->hpar[i]);
+        host_free(c->shm_own[i]);
+        host_free(c->shm_hold[i]);
+        host_free(c->shm_next[i]);
     }
     cudaGetLastError();
     delete c;
@@ -608,6 +736,7 @@ extern "C" int ckpt_export_handle(ckpt_ctx *c, void *buf, uint64_t *len) {
     b.n_slots = c->n_slots;
     b.full_copy = c->full_copy;
     b.staging_bytes = c->staging_bytes;
+    b.nonce = c->my_nonce;
     gethostname(b.host, sizeof b.host - 1);
     CUDA_TRY(cudaIpcGetMemHandle(&b.staging_h, c->staging));
     CUDA_TRY(cudaIpcGetMemHandle(&b.flags_h, c->flags));
@@ -619,30 +748,79 @@ extern "C" int ckpt_export_handle(ckpt_ctx *c, void *buf, uint64_t *len) {
 
 static inline bool device_only(const ckpt_ctx *c) { return (c->opt.flags & CKPT_OPT_DEVICE_ONLY) != 0; }
 
+static inline uint64_t parity_bytes_of(const ckpt_ctx *c) { return c->m >= 2 && c->aec ? c->Lstar / (c->m - 1) : 0; }
+static inline uint64_t shm_bytes(const ckpt_ctx *c) {
+    const uint64_t P = parity_bytes_of(c);
+    return c->Lstar + P + (c->arc ? c->Lstar + P : 0);
+}
+static inline bool use_shm(const ckpt_ctx *c) { return (c->opt.flags & CKPT_OPT_SHM_ARENA) != 0; }
+
 static int alloc_arena(ckpt_ctx *c) {
     c->completed = -1;
     c->ongoing = 0;
     if (device_only(c)) return CKPT_OK;  // the image lives in the device staging
-    const uint64_t pbytes = c->m >= 2 ? c->Lstar / (c->m - 1) : 0;
-    for (int i = 0; i < c->nbuf; ++i) {
-        int rc = host_alloc(c->hdata[i], c->Lstar);
-        if (!rc && pbytes) rc = host_alloc(c->hpar[i], pbytes);
-        if (rc) {
-            for (int k = 0; k < 2; ++k) {
-                host_free(c->hdata[k]);
-                host_free(c->hpar[k]);
+    const uint64_t pbytes = parity_bytes_of(c);
+    int rc = CKPT_OK;
+    for (int i = 0; i < c->nbuf && !rc; ++i) {
+        if (use_shm(c)) {
+            rc = shm_create(c->shm_own[i], shm_name(c->group_nonce, c->me, i), shm_bytes(c));
+            if (rc) break;
+            uint8_t *base = c->shm_own[i].p;
+            c->hdata[i] = HostBuf{base, c->Lstar, kView, true, ""};
+            if (pbytes) c->hpar[i] = HostBuf{base + c->Lstar, pbytes, kView, true, ""};
+            if (c->arc) {
+                c->harc[i] = base + c->Lstar + pbytes;
+                c->harcp[i] = pbytes ? base + 2 * c->Lstar + pbytes : nullptr;
             }
-            return rc;
+        } else {
+            rc = host_alloc(c->hdata[i], c->Lstar);
+            if (!rc && pbytes) rc = host_alloc(c->hpar[i], pbytes);
         }
+    }
+    if (rc) {
+        for (int k = 0; k < 2; ++k) {
+            host_free(c->hdata[k]);
+            host_free(c->hpar[k]);
+            host_free(c->shm_own[k]);
+        }
+        return rc;
     }
     c->completed = -1;
     c->ongoing = 0;
     return CKPT_OK;
 }
 
+// ARC push targets: the files of my holder (member me-1), pinned so that my copy engine
+// can D2H straight into the holder's ARC-copy region.  Mapped at first use (the holder
+// creates them in its own ckpt_protect).
+static int ensure_holder_mapped(ckpt_ctx *c) {
+    if (!c->arc) return CKPT_OK;
+    const uint32_t h = (c->me + c->m - 1) % c->m;
+    for (int i = 0; i < c->nbuf; ++i) {
+        if (c->shm_hold[i].p) continue;
+        int rc = shm_map(c->shm_hold[i], shm_name(c->group_nonce, h, i), shm_bytes(c), true);
+        if (rc) return rc;
+    }
+    return CKPT_OK;
+}
+
+// Member me+1's own files (recovery re-creates the ARC copy I hold from them; CPU only).
+static int ensure_next_mapped(ckpt_ctx *c) {
+    const uint32_t nx = (c->me + 1) % c->m;
+    for (int i = 0; i < c->nbuf; ++i) {
+        if (c->shm_next[i].p) continue;
+        int rc = shm_map(c->shm_next[i], shm_name(c->group_nonce, nx, i), shm_bytes(c), false);
+        if (rc) return rc;
+    }
+    return CKPT_OK;
+}
+
 static int setup_ungrouped(ckpt_ctx *c) {
     c->m = 1;
     c->me = 0;
+    c->group_nonce = c->my_nonce;
+    c->arc = false;
+    c->aec = true;
     c->Lstar = c->L;
     c->unit = c->opt.stripe_unit;
     c->peer_L[0] = c->L;
@@ -667,6 +845,11 @@ extern "C" int ckpt_protect(ckpt_ctx *c, const ckpt_group *g) {
         return rc ? rc : fail(CKPT_EUNAVAIL, "protect: a group of one has no redundancy (SPEC S.314)");
     }
     const uint32_t m = g->m;
+    const uint32_t scheme = g->scheme == CKPT_SCHEME_DEFAULT ? CKPT_SCHEME_AEC : g->scheme;
+    if (scheme > CKPT_SCHEME_ARC_AEC) return fail(CKPT_EINVAL, "protect: unknown scheme %u", g->scheme);
+    const bool arc = scheme == CKPT_SCHEME_ARC || scheme == CKPT_SCHEME_ARC_AEC;
+    if (arc && (!use_shm(c) || !c->full_copy || device_only(c)))
+        return fail(CKPT_EINVAL, "protect: ARC schemes need CKPT_OPT_SHM_ARENA and full-copy staging (n_slots = 0)");
     uint64_t Ls[CKPT_MAX_GROUP];
     if (g->transport == CKPT_GROUP_IPC) {
         if (!g->handles) return fail(CKPT_EINVAL, "protect: IPC group without handles");
@@ -687,6 +870,7 @@ extern "C" int ckpt_protect(ckpt_ctx *c, const ckpt_group *g) {
         }
         if (hb[g->my_index]->pid != (int32_t)getpid() || hb[g->my_index]->L != c->L)
             return fail(CKPT_EINVAL, "protect: my_index does not point at this context's handle");
+        c->group_nonce = hb[0]->nonce;
         for (uint32_t j = 0; j < m; ++j) {
             c->peer_L[j] = Ls[j];
             if (j == g->my_index) {
@@ -717,6 +901,8 @@ extern "C" int ckpt_protect(ckpt_ctx *c, const ckpt_group *g) {
     } else if (g->transport == CKPT_GROUP_LOCAL) {
         if (!g->members) return fail(CKPT_EINVAL, "protect: LOCAL group without members");
         if (g->members[g->my_index] != c) return fail(CKPT_EINVAL, "protect: members[my_index] is not this context");
+        if (!g->members[0]) return fail(CKPT_EINVAL, "protect: LOCAL group member 0 is NULL");
+        c->group_nonce = g->members[0]->my_nonce;
         for (uint32_t j = 0; j < m; ++j) {
             ckpt_ctx *o = g->members[j];
             if (!o || !o->registered) return fail(CKPT_ESTATE, "protect: member %u not registered", j);
@@ -752,19 +938,24 @@ extern "C" int ckpt_protect(ckpt_ctx *c, const ckpt_group *g) {
     c->transport = g->transport;
     c->Lstar = Lstar;
     c->unit = ue;
+    c->scheme = scheme;
+    c->arc = arc;
+    c->aec = scheme == CKPT_SCHEME_AEC || scheme == CKPT_SCHEME_ARC_AEC;
     // parity buffer (local)
-    if (c->full_copy) {
+    if (!c->aec) {
+        c->parity_bytes = 0;
+    } else if (c->full_copy) {
         c->parity_slot_bytes = 0;
         c->parity_bytes = std::max<uint64_t>(Lstar / (m - 1), 4096);
     } else {
         c->parity_slot_bytes = (c->slot_bytes / stripe) * ue;
         c->parity_bytes = c->parity_slot_bytes * c->n_slots;
     }
-    if (cudaMalloc(&c->parity, c->parity_bytes) != cudaSuccess) {
+    if (c->aec && cudaMalloc(&c->parity, c->parity_bytes) != cudaSuccess) {
         cudaGetLastError();
         return fail(CKPT_ENOMEM, "protect: parity buffer of %llu bytes failed", (unsigned long long)c->parity_bytes);
     }
-    if (c->opt.flags & CKPT_OPT_CE_GATHER) {
+    if (c->aec && (c->opt.flags & CKPT_OPT_CE_GATHER)) {
         c->gather_bytes = c->full_copy ? std::max<uint64_t>(Lstar, 4096) : c->parity_bytes * (m - 1);
         if (cudaMalloc(&c->gather, c->gather_bytes) != cudaSuccess) {
             cudaGetLastError();
@@ -1004,9 +1195,16 @@ static int do_rebuild_row(ckpt_ctx *c, uint64_t k, uint32_t kl, cudaStream_t s) 
 // The image's zero pad [L, L*) is structural (Q5) and never written by a D2H (which
 // covers [0, L)); after ckpt_forget poisoned a buffer, re-zero it before it commits.
 static void clean_pad(ckpt_ctx *c, int buf) {
-    if (buf < 0 || !c->pad_dirty[buf] || !c->hdata[buf].p) return;
-    if (c->Lstar > c->L) memset(c->hdata[buf].p + c->L, 0, c->Lstar - c->L);
-    c->pad_dirty[buf] = false;
+    if (buf < 0) return;
+    if (c->pad_dirty[buf] && c->hdata[buf].p) {
+        if (c->Lstar > c->L) memset(c->hdata[buf].p + c->L, 0, c->Lstar - c->L);
+        c->pad_dirty[buf] = false;
+    }
+    if (c->arc_dirty[buf] && c->harc[buf]) {  // pad of the ARC copy I hold (of member me+1)
+        const uint64_t Ln = c->peer_L[(c->me + 1) % c->m];
+        if (c->Lstar > Ln) memset(c->harc[buf] + Ln, 0, c->Lstar - Ln);
+        c->arc_dirty[buf] = false;
+    }
 }
 
 static int check_sticky(ckpt_ctx *c) {
@@ -1197,11 +1395,11 @@ static int stage_xor_all(ckpt_ctx *c) {
 }
 
 static bool xor_in_one_launch(const ckpt_ctx *c) {
-    return c->m >= 2 && single_launch(c) && !(c->opt.flags & CKPT_OPT_CE_GATHER);
+    return c->m >= 2 && c->aec && single_launch(c) && !(c->opt.flags & CKPT_OPT_CE_GATHER);
 }
 
 static int stage_xor(ckpt_ctx *c, uint64_t k) {
-    if (c->m < 2) return CKPT_OK;
+    if (c->m < 2 || !c->aec) return CKPT_OK;
     if (xor_in_one_launch(c)) return k + 1 == c->op_NB ? stage_xor_all(c) : CKPT_OK;
     const uint32_t s = slot_of(c, k);
     int rc;
@@ -1253,13 +1451,19 @@ static int stage_copy(ckpt_ctx *c, uint64_t k, bool with_parity = true) {
     if (v) {
         CUDA_TRY(cudaMemcpyAsync(c->hdata[c->ongoing].p + bb, slot_ptr(c, c->staging, k), v, cudaMemcpyDeviceToHost, c->sC));
         c->st.d2h_bytes += v;
+        if (c->arc) {  // ARC: the same bucket again, into my holder's ARC-copy region
+            uint8_t *dst = c->shm_hold[c->ongoing].p + c->Lstar + parity_bytes_of(c) + bb;
+            CUDA_TRY(cudaMemcpyAsync(dst, slot_ptr(c, c->staging, k), v, cudaMemcpyDeviceToHost, c->sC));
+            c->st.d2h_bytes += v;
+            c->st.ce_copies++;
+        }
     }
     CUDA_TRY(cudaEventRecord(c->ev_d2h_data[s], c->sC));
     return with_parity ? stage_copy_parity(c, k) : CKPT_OK;
 }
 
 static int stage_copy_parity(ckpt_ctx *c, uint64_t k) {
-    if (c->m < 2) return CKPT_OK;
+    if (c->m < 2 || !c->aec) return CKPT_OK;
     const uint32_t s = slot_of(c, k);
     const uint64_t bb = bucket_begin(c, k), be = bucket_end(c, k);
     const uint64_t pb = (be - bb) / (c->m - 1);
@@ -1268,6 +1472,12 @@ static int stage_copy_parity(ckpt_ctx *c, uint64_t k) {
         CUDA_TRY(cudaMemcpyAsync(c->hpar[c->ongoing].p + bb / (c->m - 1), parity_slot_ptr(c, k), pb,
                                  cudaMemcpyDeviceToHost, c->sC));
         c->st.d2h_bytes += pb;
+        if (c->arc) {  // ARC_AEC: my parity row into my holder's ARC copy too (Q20)
+            uint8_t *dst = c->shm_hold[c->ongoing].p + 2 * c->Lstar + parity_bytes_of(c) + bb / (c->m - 1);
+            CUDA_TRY(cudaMemcpyAsync(dst, parity_slot_ptr(c, k), pb, cudaMemcpyDeviceToHost, c->sC));
+            c->st.d2h_bytes += pb;
+            c->st.ce_copies++;
+        }
     }
     CUDA_TRY(cudaEventRecord(c->ev_d2h_par[s], c->sC));
     return CKPT_OK;
@@ -1276,7 +1486,7 @@ static int stage_copy_parity(ckpt_ctx *c, uint64_t k) {
 static int stage_finish(ckpt_ctx *c) {
     CUDA_TRY(cudaEventRecord(c->ev_pack_all, c->sP));
     CUDA_TRY(cudaStreamWaitEvent(c->sC, c->ev_pack_all, 0));
-    if (c->m >= 2) CUDA_TRY(cudaStreamWaitEvent(c->sC, c->ev_xored[slot_of(c, c->op_NB ? c->op_NB - 1 : 0)], 0));
+    if (c->m >= 2 && c->aec) CUDA_TRY(cudaStreamWaitEvent(c->sC, c->ev_xored[slot_of(c, c->op_NB ? c->op_NB - 1 : 0)], 0));
     CUDA_TRY(cudaEventRecord(c->ev_done, c->sC));
     if (c->opt.flags & CKPT_OPT_TIMING) CUDA_TRY(cudaEventRecord(c->ev_t1, c->sC));
     if (c->m >= 2) return sig_signal(c, c->sC, kDone, c->op_seq_base + (uint32_t)c->op_NB + 1, 0);
@@ -1301,6 +1511,7 @@ extern "C" int ckpt_snapshot(ckpt_ctx *c, uint64_t bucket_bytes, void *stream, u
     if (c->pending_id || c->requested) return fail(CKPT_EBUSY, "snapshot: previous snapshot %llu not waited", (unsigned long long)c->pending_id);
     if ((rc = set_dev(c))) return rc;
     if (!c->grouped && (rc = setup_ungrouped(c))) return rc;
+    if (c->arc && (rc = ensure_holder_mapped(c))) return rc;
     const uint64_t B = effective_bucket(c, bucket_bytes);
     if (!c->full_copy && B > c->slot_bytes)
         return fail(CKPT_EINVAL, "snapshot: bucket of %llu bytes exceeds slot capacity %llu", (unsigned long long)B,
@@ -1568,6 +1779,11 @@ static int rb_stage2(ckpt_ctx *c, uint64_t b, uint32_t kl) {
     return sig_signal(c, c->sX, kRel, bucket_seq(c, b), s);
 }
 
+// The buffer the survivors' completed image sits in: every member flips its double
+// buffer at the same commits, so the lost member rebuilds into that index and keeps its
+// `ongoing` in step with the group (ARC pushes rely on identical indices).
+static inline int rb_target(const ckpt_ctx *c) { return c->nbuf == 2 ? c->ongoing ^ 1 : 0; }
+
 static int rb_stage3(ckpt_ctx *c, uint64_t b, uint32_t kl) {
     if (c->me != kl) return CKPT_OK;
     const uint32_t s = slot_of(c, b);
@@ -1578,10 +1794,10 @@ static int rb_stage3(ckpt_ctx *c, uint64_t b, uint32_t kl) {
     const uint64_t v = valid_in_bucket(c->L, bb, be);
     const uint64_t pb = (be - bb) / (c->m - 1);
     if (!device_only(c) && v)
-        CUDA_TRY(cudaMemcpyAsync(c->hdata[c->ongoing].p + bb, slot_ptr(c, c->staging, b), v, cudaMemcpyDeviceToHost, c->sC));
+        CUDA_TRY(cudaMemcpyAsync(c->hdata[rb_target(c)].p + bb, slot_ptr(c, c->staging, b), v, cudaMemcpyDeviceToHost, c->sC));
     CUDA_TRY(cudaEventRecord(c->ev_d2h_data[s], c->sC));
     if (!device_only(c)) {
-        CUDA_TRY(cudaMemcpyAsync(c->hpar[c->ongoing].p + bb / (c->m - 1), parity_slot_ptr(c, b), pb, cudaMemcpyDeviceToHost, c->sC));
+        CUDA_TRY(cudaMemcpyAsync(c->hpar[rb_target(c)].p + bb / (c->m - 1), parity_slot_ptr(c, b), pb, cudaMemcpyDeviceToHost, c->sC));
         c->st.d2h_bytes += v + pb;
     }
     CUDA_TRY(cudaEventRecord(c->ev_d2h_par[s], c->sC));
@@ -1604,20 +1820,30 @@ static int rb_commit(ckpt_ctx *c, uint32_t kl, uint64_t version) {
         return rc;
     }
     if (c->me == kl) {
-        clean_pad(c, c->ongoing);
-        c->completed = c->ongoing;
+        clean_pad(c, rb_target(c));
+        c->completed = rb_target(c);
         c->completed_id = version;
-        if (c->nbuf == 2) c->ongoing ^= 1;
     }
     c->st.rebuilds++;
     return CKPT_OK;
 }
 
+static int rebuild_aec(ckpt_ctx *c, int32_t lost, void *stream);
+extern "C" int ckpt_recover(ckpt_ctx *c, uint32_t lost_mask, void *stream);
+
 extern "C" int ckpt_rebuild(ckpt_ctx *c, int32_t lost, void *stream) {
+    if (!c) return fail(CKPT_EINVAL, "rebuild: null");
+    // ARC schemes also re-create the ARC copy the lost member held: the general path
+    if (c->grouped && c->arc && lost >= 0 && (uint32_t)lost < c->m) return ckpt_recover(c, 1u << lost, stream);
+    return rebuild_aec(c, lost, stream);
+}
+
+static int rebuild_aec(ckpt_ctx *c, int32_t lost, void *stream) {
     if (!c) return fail(CKPT_EINVAL, "rebuild: null");
     if (!c->registered || !c->grouped) return fail(CKPT_ESTATE, "rebuild: not protected");
     if (c->m < 2) return fail(CKPT_EUNRECOVERABLE, "rebuild: a group of one has no redundancy (P.460)");
     if (lost < 0 || (uint32_t)lost >= c->m) return fail(CKPT_EINVAL, "rebuild: lost rank %d out of range", lost);
+    if (!c->aec) return fail(CKPT_EUNRECOVERABLE, "rebuild: the scheme has no parity");
     int rc = check_sticky(c);
     if (rc) return rc;
     if (c->pending_id || c->requested) return fail(CKPT_ESTATE, "rebuild: a snapshot is in flight");
@@ -1689,6 +1915,96 @@ extern "C" int ckpt_rebuild(ckpt_ctx *c, int32_t lost, void *stream) {
     return rb_commit(c, kl, c->me == kl ? c->next_id - 1 : c->completed_id);
 }
 
+// ------------------------------------------------------------------ recover (1-2 losses)
+// The oracle's oracle_recover, step by step: (1) ARC restore of every lost member whose
+// holder survived (the member copies its image out of the holder's shared file), (2)
+// AEC rebuild of one remaining loss (collective, rebuild_aec), (3) every lost member
+// re-creates the ARC copy it holds from member me+1's completed image.
+static inline uint32_t holder_of(const ckpt_ctx *c, uint32_t x) { return (x + c->m - 1) % c->m; }
+
+static int recover_plan(const ckpt_ctx *c, uint32_t mask, int32_t *remaining) {
+    *remaining = -1;
+    const int nlost = __builtin_popcount(mask);
+    if (nlost > 2) return fail(CKPT_EUNRECOVERABLE, "recover: %d losses (at most 2 are tolerated, P.507)", nlost);
+    int left = 0;
+    for (uint32_t x = 0; x < c->m; ++x) {
+        if (!(mask & (1u << x))) continue;
+        if (c->arc && !(mask & (1u << holder_of(c, x)))) continue;  // restored by ARC
+        ++left;
+        *remaining = (int32_t)x;
+    }
+    if (left > 1 || (left == 1 && !c->aec))
+        return fail(CKPT_EUNRECOVERABLE, "recover: losses 0x%x exceed what scheme %u restores", mask, c->scheme);
+    return CKPT_OK;
+}
+
+static int recover_step1(ckpt_ctx *c, uint32_t mask, uint64_t version) {
+    if (!(mask & (1u << c->me)) || !c->arc || (mask & (1u << holder_of(c, c->me)))) return CKPT_OK;
+    int rc = ensure_holder_mapped(c);
+    if (rc) return rc;
+    const int idx = rb_target(c);
+    const uint64_t P = parity_bytes_of(c);
+    parallel_memcpy(c->hdata[idx].p, c->shm_hold[idx].p + c->Lstar + P, c->Lstar);
+    if (c->aec) parallel_memcpy(c->hpar[idx].p, c->shm_hold[idx].p + 2 * c->Lstar + P, P);
+    c->pad_dirty[idx] = false;  // the holder's copy carries the image's zero pad
+    c->completed = idx;
+    c->completed_id = version;
+    c->st.h2d_bytes += 0;
+    return CKPT_OK;
+}
+
+static int recover_step3(ckpt_ctx *c, uint32_t mask) {
+    if (!(mask & (1u << c->me)) || !c->arc) return CKPT_OK;
+    int rc = ensure_next_mapped(c);
+    if (rc) return rc;
+    const int idx = c->completed;
+    if (idx < 0) return fail(CKPT_ESTATE, "recover: member %u has no completed image after restore", c->me);
+    const uint64_t P = parity_bytes_of(c);
+    parallel_memcpy(c->harc[idx], c->shm_next[idx].p, c->Lstar);  // member me+1's data + pad
+    if (c->aec) parallel_memcpy(c->harcp[idx], c->shm_next[idx].p + c->Lstar, P);
+    c->arc_dirty[idx] = false;
+    return CKPT_OK;
+}
+
+extern "C" int ckpt_recover(ckpt_ctx *c, uint32_t mask, void *stream) {
+    if (!c) return fail(CKPT_EINVAL, "recover: null");
+    if (!c->registered || !c->grouped) return fail(CKPT_ESTATE, "recover: not protected");
+    if (c->m < 2) return fail(CKPT_EUNRECOVERABLE, "recover: a group of one has no redundancy (P.460)");
+    if (mask >> c->m) return fail(CKPT_EINVAL, "recover: lost mask 0x%x names members >= m", mask);
+    if (device_only(c) && c->arc) return fail(CKPT_EINVAL, "recover: ARC needs a host arena");
+    int rc = check_sticky(c);
+    if (rc) return rc;
+    if (c->pending_id || c->requested) return fail(CKPT_ESTATE, "recover: a snapshot is in flight");
+    int32_t rem;
+    if ((rc = recover_plan(c, mask, &rem))) return rc;
+    if (!mask) return CKPT_OK;
+    if (!(mask & (1u << c->me)) && c->completed < 0)
+        return fail(CKPT_ENOSNAP, "recover: survivor %u has no completed image", c->me);
+    if (c->transport == CKPT_GROUP_LOCAL) {
+        c->recover_requested = true;
+        c->recover_mask = mask;
+        c->recover_stream = stream;
+        for (uint32_t j = 0; j < c->m; ++j)
+            if (!c->members[j]->recover_requested) return CKPT_OK;  // run by the last member
+        uint64_t version = 0;
+        for (uint32_t j = 0; j < c->m; ++j) {
+            ckpt_ctx *o = c->members[j];
+            if (o->recover_mask != mask) return fail(CKPT_EINVAL, "recover: members disagree on the lost mask");
+            if (!(mask & (1u << j))) version = std::max(version, o->completed_id);
+        }
+        for (uint32_t j = 0; j < c->m && !rc; ++j) rc = recover_step1(c->members[j], mask, version);
+        for (uint32_t j = 0; j < c->m && !rc && rem >= 0; ++j)
+            rc = rebuild_aec(c->members[j], rem, c->members[j]->recover_stream);
+        for (uint32_t j = 0; j < c->m && !rc; ++j) rc = recover_step3(c->members[j], mask);
+        for (uint32_t j = 0; j < c->m; ++j) c->members[j]->recover_requested = false;
+        set_dev(c);
+        return rc;
+    }
+    if ((rc = recover_step1(c, mask, c->next_id - 1))) return rc;
+    if (rem >= 0 && (rc = rebuild_aec(c, rem, stream))) return rc;
+    return recover_step3(c, mask);
+}
+
 // ------------------------------------------------------------------ misc ------------
 extern "C" int ckpt_forget(ckpt_ctx *c, uint8_t poison) {
     if (!c) return fail(CKPT_EINVAL, "forget: null");
@@ -1704,6 +2020,11 @@ extern "C" int ckpt_forget(ckpt_ctx *c, uint8_t poison) {
         if (c->hdata[i].p) memset(c->hdata[i].p, poison, c->Lstar);
         if (c->hpar[i].p && c->m >= 2) memset(c->hpar[i].p, poison, c->Lstar / (c->m - 1));
         c->pad_dirty[i] = c->hdata[i].p != nullptr;
+        if (c->harc[i]) {  // the ARC copy this member holds is lost with it
+            memset(c->harc[i], poison, c->Lstar);
+            if (c->harcp[i]) memset(c->harcp[i], poison, parity_bytes_of(c));
+            c->arc_dirty[i] = true;
+        }
     }
     c->completed = -1;
     c->completed_id = 0;
@@ -1712,15 +2033,25 @@ extern "C" int ckpt_forget(ckpt_ctx *c, uint8_t poison) {
 
 extern "C" int ckpt_host_view(const ckpt_ctx *c, int which, const void **data, uint64_t *dlen, const void **par,
                               uint64_t *plen) {
-    if (!c || (which != 0 && which != 1)) return fail(CKPT_EINVAL, "host_view: bad args");
+    if (!c || which < 0 || which > 3) return fail(CKPT_EINVAL, "host_view: bad args");
+    if (which >= 2) {
+        if (!c->grouped || !c->arc) return fail(CKPT_EINVAL, "host_view: no ARC copy (scheme without ARC)");
+        int idx = which == 2 ? c->completed : c->ongoing;
+        if (idx < 0) return fail(CKPT_ENOSNAP, "host_view: no completed snapshot");
+        if (data) *data = c->harc[idx];
+        if (dlen) *dlen = c->Lstar;
+        if (par) *par = c->harcp[idx];
+        if (plen) *plen = c->harcp[idx] ? parity_bytes_of(c) : 0;
+        return CKPT_OK;
+    }
     if (!c->grouped) return fail(CKPT_ENOSNAP, "host_view: no host arena yet");
     if (device_only(c)) return fail(CKPT_EINVAL, "host_view: DEVICE_ONLY context has no host image");
     int idx = which == 0 ? c->completed : c->ongoing;
     if (idx < 0) return fail(CKPT_ENOSNAP, "host_view: no completed snapshot");
     if (data) *data = c->hdata[idx].p;
     if (dlen) *dlen = c->Lstar;
-    if (par) *par = c->m >= 2 ? c->hpar[idx].p : nullptr;
-    if (plen) *plen = c->m >= 2 ? c->Lstar / (c->m - 1) : 0;
+    if (par) *par = c->m >= 2 && c->aec ? c->hpar[idx].p : nullptr;
+    if (plen) *plen = c->m >= 2 && c->aec ? c->Lstar / (c->m - 1) : 0;
     return CKPT_OK;
 }
 

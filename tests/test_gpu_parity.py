@@ -447,3 +447,92 @@ def test_no_writes_outside_tensors(torch, C, flags, n_slots):
     finally:
         for c in ctxs:
             C.ckpt_destroy(c)
+
+
+def _arc_expect(states, Lstar, unit, scheme):
+    Ds = [oracle_image(specs, j, Lstar)[0] for j, (specs, _) in enumerate(states)]
+    Ps = oracle.encode_all(Ds, unit) if scheme != 2 else [None] * len(Ds)
+    MDs = [oracle.arc_copy(Ds, i) for i in range(len(Ds))]
+    MPs = [Ps[(i + 1) % len(Ds)] for i in range(len(Ds))]
+    return Ds, Ps, MDs, MPs
+
+
+def _check_all_views(C, ctxs, exp, scheme, what):
+    Ds, Ps, MDs, MPs = exp
+    for j, c in enumerate(ctxs):
+        d, p = C.ckpt_host_view(c, 0, copy=True)
+        assert_bytes_equal(d, Ds[j], f"{what}: member {j} data")
+        if scheme != 2:
+            assert_bytes_equal(p, Ps[j], f"{what}: member {j} parity")
+        ad, ap = C.ckpt_host_view(c, 2, copy=True)
+        assert_bytes_equal(ad, MDs[j], f"{what}: member {j} ARC copy of {(j + 1) % len(ctxs)}")
+        if scheme == 3:
+            assert_bytes_equal(ap, MPs[j], f"{what}: member {j} ARC parity copy")
+
+
+@pytest.mark.parametrize("m,scheme", [(2, 2), (3, 2), (4, 2), (3, 3), (4, 3), (5, 3), (8, 3)])
+def test_arc_schemes_snapshot_and_every_recovery(torch, C, m, scheme):
+    """ARC (ring copies, 2 W_n/m) and ARC+AEC (collaborative, any two
+    losses for m >= 3) -- host images, parity rows and ARC copies bit-exact against the
+    oracle; every single loss and (ARC+AEC) every pair recovered and reloaded."""
+    import itertools
+
+    from synth.gpu import fill_state
+    unit = 4096
+    states = [tiny(j, n=5 + j % 3, misalign=1) for j in range(m)]
+    ctxs = [make_ctx(C, st, n_slots=0, bucket_bytes=1 << 16, stripe_unit=unit, flags=0x40) for st in states]
+    try:
+        C.protect_local(ctxs, scheme=scheme)
+        snapshot_group(C, ctxs)
+        g = C.ckpt_geometry(ctxs[0])
+        exp = _arc_expect(states, g["L_star"], g["unit"], scheme)
+        _check_all_views(C, ctxs, exp, scheme, "snapshot")
+        cases = [(x,) for x in range(m)]
+        if scheme == 3:
+            cases += list(itertools.combinations(range(m), 2))
+        for lost in cases:
+            mask = sum(1 << x for x in lost)
+            for j, (_, ts) in enumerate(states):
+                fill_state(ts, j, seed=11 + mask, xor_mode=1)
+            for x in lost:
+                C.ckpt_forget(ctxs[x], 0xA5)
+                for t in states[x][1]:
+                    t.view(torch.uint8).fill_(0xA5)
+            for c in ctxs:
+                C.ckpt_recover(c, mask)
+            _check_all_views(C, ctxs, exp, scheme, f"after losing {lost}")
+            for c in ctxs:
+                C.ckpt_load(c)
+            torch.cuda.synchronize()
+            for j, (specs, ts) in enumerate(states):
+                for t, (x, w) in enumerate(zip(ts, oracle_tensor_bytes(specs, j))):
+                    assert_bytes_equal(tensor_bytes(x), w, f"lost {lost}: member {j} tensor {t}")
+        # a snapshot after the drills still commits the same images everywhere
+        snapshot_group(C, ctxs)
+        _check_all_views(C, ctxs, exp, scheme, "snapshot after drills")
+        if m >= 3:  # beyond the scheme: consistent refusal, nothing changes
+            bad = 0b11 if scheme == 2 else 0b111
+            for c in ctxs:
+                with pytest.raises(C.CkptError) as e:
+                    C.ckpt_recover(c, bad)
+                assert e.value.code == C.CKPT_EUNRECOVERABLE
+    finally:
+        for c in ctxs:
+            C.ckpt_destroy(c)
+
+
+def test_shm_arena_aec_matches_anon(torch, C):
+    """The shared-memory arena (CKPT_OPT_SHM_ARENA) holds the same images as the
+    anonymous one for the default AEC scheme."""
+    states, ctxs = make_group(torch, C, 4, 4096, flags=0x40)
+    try:
+        snapshot_group(C, ctxs)
+        g = C.ckpt_geometry(ctxs[0])
+        Ds, Ps = expected_group(states, g["L_star"], g["unit"])
+        for j, c in enumerate(ctxs):
+            d, p = C.ckpt_host_view(c, 0, copy=True)
+            assert_bytes_equal(d, Ds[j], f"rank {j} data")
+            assert_bytes_equal(p, Ps[j], f"rank {j} parity")
+    finally:
+        for c in ctxs:
+            C.ckpt_destroy(c)

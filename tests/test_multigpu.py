@@ -226,3 +226,114 @@ def test_ipc_full_size_sampled(config):
                 p.kill()
     for rank, ok, _ in res:
         assert all(ok), (rank, ok)
+
+
+def _worker_arc(rank, world, port, q, scheme):
+    try:
+        os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank), WORLD_SIZE=str(world))
+        import itertools
+
+        import torch
+        import torch.distributed as dist
+
+        import oracle
+        import synth
+        from paper_2310_12670_b200 import ckpt as C
+        from synth.gpu import descriptors, fill_state, make_rank_state
+
+        torch.cuda.set_device(rank)
+        dev = torch.device("cuda", rank)
+        dist.init_process_group("nccl", device_id=dev)
+        specs, ts = make_rank_state("tiny_8", rank, dev, misalign=1)
+        ctx = C.ckpt_create(rank, C.ckpt_options_default(stripe_unit=4096, n_slots=0, bucket_bytes=1 << 16,
+                                                         flags=C.CKPT_OPT_SHM_ARENA))
+        C.ckpt_register(ctx, descriptors(ts, specs))
+        C.protect_ipc(ctx, scheme=scheme)
+        g = C.ckpt_geometry(ctx)
+        imgs = []
+        for j in range(world):
+            sp = synth.config_tensors("tiny_8", j)
+            tb = [synth.fill(synth.SEED, j, t, s.nbytes) for t, s in enumerate(sp)]
+            off, _ = oracle.layout([s.nbytes for s in sp])
+            imgs.append(oracle.pack(tb, off, g["L_star"]))
+        Ps = oracle.encode_all(imgs, g["unit"]) if scheme != 2 else None
+        nxt = (rank + 1) % world
+
+        def views_ok():
+            d, p = C.ckpt_host_view(ctx, 0, copy=True)
+            ad, ap = C.ckpt_host_view(ctx, 2, copy=True)
+            ok = np.array_equal(d, imgs[rank]) and np.array_equal(ad, imgs[nxt])
+            if scheme != 2:
+                ok = ok and np.array_equal(p, Ps[rank])
+            if scheme == 3:
+                ok = ok and np.array_equal(ap, Ps[nxt])
+            return bool(ok)
+
+        sid = C.ckpt_snapshot(ctx)
+        C.ckpt_wait(ctx, sid)
+        ok = [views_ok()]
+        cases = [(x,) for x in range(world)]
+        if scheme == 3 and world >= 3:
+            cases += list(itertools.combinations(range(world), 2))
+        for lost in cases:
+            mask = sum(1 << x for x in lost)
+            fill_state(ts, rank, seed=5 + mask, xor_mode=1)
+            if rank in lost:
+                C.ckpt_forget(ctx, 0xA5)
+                for t in ts:
+                    t.view(torch.uint8).fill_(0xA5)
+            dist.barrier()
+            C.ckpt_recover(ctx, mask)
+            C.ckpt_load(ctx)
+            torch.cuda.synchronize()
+            dist.barrier()
+            good = views_ok()
+            for t, x in enumerate(ts):
+                got = x.contiguous().view(torch.uint8).cpu().numpy()
+                good = good and np.array_equal(got, synth.fill(synth.SEED, rank, t, specs[t].nbytes))
+            ok.append(bool(good))
+        sid = C.ckpt_snapshot(ctx)
+        C.ckpt_wait(ctx, sid)
+        ok.append(views_ok())
+        dist.barrier()
+        C.ckpt_destroy(ctx)
+        dist.barrier()
+        dist.destroy_process_group()
+        q.put((rank, ok, None))
+    except Exception:
+        q.put((rank, None, traceback.format_exc()))
+
+
+@pytest.mark.parametrize("scheme", [2, 3])
+def test_ipc_arc_schemes(scheme):
+    """ARC and ARC+AEC across processes: pushes into the holder's shared-memory arena,
+    every single loss (and every pair for ARC+AEC) recovered, bit-exact."""
+    world = min(_world(), 4)
+    import queue
+    import time
+
+    import torch.multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    ps = [ctx.Process(target=_worker_arc, args=(r, world, port, q, scheme)) for r in range(world)]
+    for p in ps:
+        p.start()
+    res, t0 = [], time.time()
+    try:
+        while len(res) < world:
+            try:
+                r = q.get(timeout=5)
+            except queue.Empty:
+                assert all(p.exitcode in (None, 0) for p in ps), "worker died"
+                assert time.time() - t0 < 300, "timed out"
+                continue
+            assert r[2] is None, r[2]
+            res.append(r)
+    finally:
+        for p in ps:
+            p.join(30)
+            if p.is_alive():
+                p.kill()
+    for rank, ok, _ in res:
+        assert all(ok), (rank, ok)
