@@ -46,6 +46,8 @@ def parse():
     p.add_argument("--device-only", action="store_true",
                    help="CKPT_OPT_DEVICE_ONLY: device-side protect only (pack + parity into HBM, no D2H)")
     p.add_argument("--max-ctas", type=int, default=0, help="CTA budget of a pack/XOR launch (0 = 2 x SMs)")
+    p.add_argument("--scheme", default="aec", choices=["aec", "arc", "arc_aec"],
+                   help="protection: AEC parity (default), ARC ring copies, or both (collaborative)")
     p.add_argument("--no-corun", action="store_true", help="skip the co-running GEMM measurement")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu-baseline", action="store_true")
@@ -218,16 +220,24 @@ def main():
              | (C.CKPT_OPT_DEVICE_ONLY if a.device_only else 0))
     if a.device_only:
         a.n_slots = 0
-    # pinned host arena: 2 x (L + L/(m-1)) per rank; fall back to one buffer if the node's
-    # available memory (all ranks together, +25% headroom) would not hold two
+    # pinned host arena per rank and buffer: L + L/(m-1) (AEC) [+ the ARC copy of the
+    # neighbour: L (+ L/(m-1))]; fall back to one buffer if the node's available memory
+    # (and /dev/shm for the ARC schemes), all ranks together +25%, would not hold two
+    scheme = {"aec": C.CKPT_SCHEME_AEC, "arc": C.CKPT_SCHEME_ARC, "arc_aec": C.CKPT_SCHEME_ARC_AEC}[a.scheme]
+    P = S // (world - 1) if world > 1 and a.scheme != "arc" else 0
+    per_buf = S + P + ((S + P) if a.scheme != "aec" and world > 1 else 0)
     host_buffers = 2
     try:
         avail = int([l for l in open("/proc/meminfo") if l.startswith("MemAvailable")][0].split()[1]) * 1024
-        need = world * 2 * (S + (S // (world - 1) if world > 1 else 0)) * 1.25 + world * (4 << 30)
-        if need > avail:
+        if a.scheme != "aec":
+            st_shm = os.statvfs("/dev/shm")
+            avail = min(avail, st_shm.f_bavail * st_shm.f_frsize)
+        if world * 2 * per_buf * 1.25 + world * (4 << 30) > avail:
             host_buffers = 1
     except Exception:
         pass
+    if a.scheme != "aec":
+        flags |= C.CKPT_OPT_SHM_ARENA
     opts = C.ckpt_options_default(n_slots=a.n_slots, bucket_bytes=a.bucket, stripe_unit=a.unit, flags=flags,
                                   max_ctas=a.max_ctas, host_buffers=host_buffers)
     ctx = C.ckpt_create(local, opts)
@@ -236,7 +246,7 @@ def main():
                                                   "local_world": world, "tp_rank": rank, "tp_size": 8,
                                                   "pp_rank": 0, "pp_size": 1, "dp_rank": 0, "dp_size": 1})
     if world > 1:
-        C.protect_ipc(ctx)
+        C.protect_ipc(ctx, scheme=scheme)
     else:
         C.ckpt_protect(ctx, 1, 0)  # EUNAVAIL: snapshot only, allocates the host arena
     t_setup = time.perf_counter() - t_setup
@@ -387,6 +397,7 @@ def main():
                        "m": m, "L_star": g["L_star"], "stripe_unit": g["unit"], "bucket_bytes": a.bucket,
                        "n_slots": a.n_slots, "pack": a.pack, "gather": a.gather, "device_only": a.device_only,
                        "max_ctas": a.max_ctas or "2 x SMs", "host_buffers": host_buffers,
+                       "scheme": a.scheme,
                        "l2": f"inputs {S / 1e9:.2f} GB/GPU >> 126 MB L2; no flush needed"},
             "per_gpu_gbs": round(value / N, 3),
             "host_link": None if a.device_only else {

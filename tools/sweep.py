@@ -32,6 +32,8 @@ def main():
     p.add_argument("--drill", action="store_true")
     p.add_argument("--device-only", action="store_true")
     p.add_argument("--lost", default="")
+    p.add_argument("--scheme", type=int, default=0, help="CKPT_SCHEME_*: 1 AEC, 2 ARC, 3 ARC+AEC")
+    p.add_argument("--host-buffers", type=int, default=2)
     a = p.parse_args()
     import torch
     import torch.distributed as dist
@@ -61,12 +63,15 @@ def main():
     S = sum(s.nbytes for s in specs)
     for bmib in [int(x) for x in a.buckets.split(",")]:
         flags = a.flags | C.CKPT_OPT_TIMING | (C.CKPT_OPT_DEVICE_ONLY if a.device_only else 0)
+        if a.scheme in (2, 3):
+            flags |= C.CKPT_OPT_SHM_ARENA
         n_slots = 0 if a.device_only else a.n_slots
         ctx = C.ckpt_create(local, C.ckpt_options_default(bucket_bytes=bmib << 20, n_slots=n_slots,
-                                                          stripe_unit=a.unit, flags=flags))
+                                                          stripe_unit=a.unit, flags=flags,
+                                                          host_buffers=a.host_buffers))
         C.ckpt_register(ctx, descriptors(ts, specs))
         if world > 1:
-            C.protect_ipc(ctx)
+            C.protect_ipc(ctx, scheme=a.scheme)
         else:
             C.ckpt_protect(ctx, 1, 0)
         g = C.ckpt_geometry(ctx)
@@ -94,18 +99,19 @@ def main():
                "xor_nvlink_gbs": round(st["xor_bytes_in"] / max(st["xor_ms"], 1e-9) / 1e6, 1),
                "launches_per_snapshot": (st["pack_launches"] + st["xor_launches"]) // a.reps}
         if a.drill and g["m"] >= 2:
-            lost = [int(x) for x in a.lost.split(",")] if a.lost else [0, g["m"] - 1]
+            lost = [tuple(int(y) for y in x.split("+")) for x in a.lost.split(",")] if a.lost else [(0,), (g["m"] - 1,)]
             C.ckpt_stats_reset(ctx)
             for k in lost:
-                fill_state(ts, rank, seed=999 + k, xor_mode=1)  # later steps mutate everything
-                if rank == k:
+                mask = sum(1 << x for x in k)
+                fill_state(ts, rank, seed=999 + mask, xor_mode=1)  # later steps mutate everything
+                if rank in k:
                     C.ckpt_forget(ctx, 0xA5)
                     for x in ts:
                         x.view(torch.uint8).fill_(0xA5)
                 bar()
                 torch.cuda.synchronize()
                 t0 = time.perf_counter()
-                C.ckpt_rebuild(ctx, k)
+                C.ckpt_recover(ctx, mask)
                 t1 = time.perf_counter()
                 C.ckpt_load(ctx)
                 torch.cuda.synchronize()
@@ -125,7 +131,7 @@ def main():
                 kgbs = (srb["rebuild_bytes_in"] + srb["rebuild_bytes_out"]) / max(srb["rebuild_ms"], 1e-9) / 1e6
                 rec.setdefault("drill", []).append({"lost": k, "rebuild_ms": round(rb * 1e3, 2), "load_ms": round(ld * 1e3, 2),
                                                     "bit_exact_sampled": okall,
-                                                    "rank0_rebuild_kernel_gbs": round(kgbs, 1) if rank != k else None,
+                                                    "rank0_rebuild_kernel_gbs": round(kgbs, 1) if rank not in k else None,
                                                     "rank0_rebuild_launches": srb["rebuild_launches"]})
                 C.ckpt_stats_reset(ctx)
         if rank == 0:
