@@ -93,7 +93,15 @@ typedef struct ckpt_options {
                                = the device's LEAST priority (so training runs first)   */
     uint32_t max_ctas;      /* CTA budget of one pack/xor launch; 0 = 2 x SM count      */
     uint32_t flags;         /* CKPT_OPT_*                                               */
-    uint32_t reserved[7];
+    uint32_t reserved0;
+    uint64_t arena_key;     /* with CKPT_OPT_SHM_ARENA: 0 = private arena (unlinked at
+                               destroy); != 0 = PERSISTENT arena named by this key and
+                               the member index (= layout.local_rank): it outlives the
+                               process like the paper's tmpfs copies (P.553-555), and a
+                               process registering the same key, layout and geometry
+                               re-attaches the last committed image (ckpt_load restores
+                               it).  Remove it with ckpt_arena_unlink.                   */
+    uint32_t reserved[4];
 } ckpt_options;
 
 /* ---- registered tensors and layout -------------------------------------------------- */
@@ -297,6 +305,10 @@ int ckpt_plan_layout(const uint64_t *nbytes, uint64_t n, uint32_t align,
 /* Host-only: L* and effective u for a group with packed lengths Lj[0..m). */
 int ckpt_plan_common(const uint64_t *Lj, uint32_t m, uint64_t unit, uint64_t *L_star,
                      uint64_t *unit_eff);
+
+/* Remove the persistent arena of `key` (members [0, m), host buffers [0, nbuf)) from
+ * /dev/shm.  Host-only; missing objects are ignored. */
+int ckpt_arena_unlink(uint64_t key, uint32_t m, uint32_t nbuf);
 
 /* Library version string, e.g. "reft-ckpt 0.1 sm_100a". */
 const char *ckpt_version(void);

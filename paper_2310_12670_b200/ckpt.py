@@ -54,7 +54,7 @@ _vp = ctypes.c_void_p
 class ckpt_options(ctypes.Structure):
     _fields_ = [("struct_size", _u32), ("align", _u32), ("stripe_unit", _u64), ("bucket_bytes", _u64),
                 ("n_slots", _u32), ("host_buffers", _u32), ("priority", _i32), ("max_ctas", _u32),
-                ("flags", _u32), ("reserved", _u32 * 7)]
+                ("flags", _u32), ("reserved0", _u32), ("arena_key", _u64), ("reserved", _u32 * 4)]
 
 
 class ckpt_tensor(ctypes.Structure):
@@ -126,6 +126,7 @@ def lib():
             "ckpt_plan_layout": (ctypes.c_int, [_vp, _u64, _u32, _vp, ctypes.POINTER(_u64)]),
             "ckpt_plan_common": (ctypes.c_int, [_vp, _u32, _u64, ctypes.POINTER(_u64), ctypes.POINTER(_u64)]),
             "ckpt_version": (ctypes.c_char_p, []),
+            "ckpt_arena_unlink": (ctypes.c_int, [_u64, _u32, _u32]),
         }
         for name, (res, args) in sig.items():
             f = getattr(L, name)
@@ -298,6 +299,10 @@ def ckpt_get_stats(ctx: int) -> dict:
 
 def ckpt_stats_reset(ctx: int) -> None:
     _check(lib().ckpt_stats_reset(ctx), "ckpt_stats_reset")
+
+
+def ckpt_arena_unlink(key: int, m: int, nbuf: int = 2) -> None:
+    _check(lib().ckpt_arena_unlink(key, m, nbuf), "ckpt_arena_unlink")
 
 
 def ckpt_plan_layout(nbytes: Sequence[int], align: int = 256):

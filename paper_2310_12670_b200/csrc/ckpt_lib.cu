@@ -109,6 +109,8 @@ struct HandleBlob {  // exported by ckpt_export_handle; fixed layout, <= CKPT_HA
     uint32_t full_copy;
     uint64_t staging_bytes;
     uint64_t nonce;         // random per context; member 0's names the group's shm arena
+    uint64_t arena_key;     // persistent arena key (0 = none); all members must agree
+    uint64_t attached_id;   // committed snapshot id found in this member's persistent arena
     char host[64];
     cudaIpcMemHandle_t staging_h;
     cudaIpcMemHandle_t flags_h;
@@ -137,6 +139,15 @@ struct HostBuf {
     bool registered = false;
     std::string name;  // shm object name (kShmOwn: unlinked at free)
 };
+// Persistent-arena metadata (its own 4 KiB shm object per member): geometry + the
+// committed version, published with one atomic 64-bit store after the image is complete.
+struct ArenaMeta {
+    uint32_t magic, version;
+    uint64_t L, Lstar, unit;
+    uint32_t m, me, scheme, nbuf, align, reserved;
+    uint64_t state;  // (completed_id << 8) | (completed_index + 1); 0 = nothing committed
+};
+constexpr uint32_t kMetaMagic = 0x41464552u;  // "REFA"
 }  // namespace
 
 struct ckpt_ctx {
@@ -193,6 +204,13 @@ struct ckpt_ctx {
     HostBuf shm_own[2], shm_hold[2], shm_next[2];  // mine, my ARC holder's, member me+1's
     uint8_t *harc[2] = {}, *harcp[2] = {};          // the ARC copy I hold (of member me+1)
     bool arc_dirty[2] = {false, false};             // its zero pad was poisoned
+    // persistent arena (options.arena_key != 0)
+    HostBuf meta_buf;
+    ArenaMeta *meta = nullptr;
+    uint32_t arena_member = 0;
+    uint64_t attached_id = 0;  // committed id found at registration (0 = none)
+    int attached_idx = -1;
+    uint64_t group_version = 0;  // max committed id over the group at ckpt_protect
     int nbuf = 2;
     int completed = -1, ongoing = 0;
     bool pad_dirty[2] = {false, false};  // zero pad [L, L*) overwritten by ckpt_forget
@@ -422,6 +440,50 @@ static int shm_map(HostBuf &b, const std::string &name, uint64_t bytes, bool reg
     return CKPT_OK;
 }
 
+// Re-attach an existing shared-memory object of at least `bytes` (persistent arena): the
+// contents are kept (MAP_POPULATE touches the pages without writing them).
+static int shm_attach(HostBuf &b, const std::string &name, uint64_t bytes, bool reg) {
+    b = HostBuf{};
+    const uint64_t len = align_up(std::max<uint64_t>(bytes, 1), 2ull << 20);
+    int fd = shm_open(name.c_str(), O_RDWR, 0600);
+    if (fd < 0) return CKPT_ENOSNAP;
+    struct stat st;
+    if (fstat(fd, &st) != 0 || (uint64_t)st.st_size < len) {
+        close(fd);
+        return CKPT_ENOSNAP;
+    }
+    void *p = mmap(nullptr, len, PROT_READ | PROT_WRITE, MAP_SHARED | MAP_POPULATE, fd, 0);
+    close(fd);
+    if (p == MAP_FAILED) return fail(CKPT_ENOMEM, "mmap(%s) failed: %s", name.c_str(), strerror(errno));
+    if (reg && cudaHostRegister(p, len, cudaHostRegisterPortable) != cudaSuccess) {
+        cudaGetLastError();
+        munmap(p, len);
+        return fail(CKPT_ENOMEM, "cudaHostRegister of persistent shm %s failed", name.c_str());
+    }
+    b.p = (uint8_t *)p;
+    b.bytes = len;
+    b.kind = kShmPeer;  // persistent: unmapped but never unlinked by this process
+    b.registered = reg;
+    b.name = name;
+    return CKPT_OK;
+}
+
+static std::string meta_name(uint64_t key, uint32_t member) {
+    char s[64];
+    snprintf(s, sizeof s, "/reft-%016llx-%u-meta", (unsigned long long)key, member);
+    return s;
+}
+
+extern "C" int ckpt_arena_unlink(uint64_t key, uint32_t m, uint32_t nbuf) {
+    if (key == 0 || m == 0 || m > CKPT_MAX_GROUP || nbuf == 0 || nbuf > 2)
+        return fail(CKPT_EINVAL, "arena_unlink: bad args");
+    for (uint32_t j = 0; j < m; ++j) {
+        shm_unlink(meta_name(key, j).c_str());
+        for (uint32_t b = 0; b < nbuf; ++b) shm_unlink(shm_name(key, j, (int)b).c_str());
+    }
+    return CKPT_OK;
+}
+
 static void host_free(HostBuf &b) {
     if (!b.p) return;
     switch (b.kind) {
@@ -610,6 +672,7 @@ extern "C" int ckpt_destroy(ckpt_ctx *c) {
         host_free(c->shm_hold[i]);
         host_free(c->shm_next[i]);
     }
+    host_free(c->meta_buf);
     cudaGetLastError();
     delete c;
     return CKPT_OK;
@@ -696,6 +759,22 @@ extern "C" int ckpt_register(ckpt_ctx *c, const ckpt_tensor *t, uint64_t n, cons
     c->segs = std::move(segs);
     c->L = L;
     if (layout) c->layout = *layout;
+    if ((c->opt.flags & CKPT_OPT_SHM_ARENA) && c->opt.arena_key) {
+        // persistent arena: look for this member's committed image (REFT-load after an
+        // elastic restart, P.551-555).  Geometry is checked again at ckpt_protect.
+        c->arena_member = layout ? (uint32_t)std::max(0, layout->local_rank) : 0;
+        HostBuf mb;
+        if (shm_attach(mb, meta_name(c->opt.arena_key, c->arena_member), 4096, false) == CKPT_OK) {
+            ArenaMeta *mt = (ArenaMeta *)mb.p;
+            const uint64_t st = __atomic_load_n(&mt->state, __ATOMIC_ACQUIRE);
+            if (mt->magic == kMetaMagic && mt->L == L && st != 0) {
+                c->attached_id = st >> 8;
+                c->attached_idx = (int)(st & 0xff) - 1;
+            }
+            c->meta_buf = mb;
+            c->meta = mt;
+        }
+    }
     c->registered = true;
     return CKPT_OK;
 }
@@ -737,6 +816,8 @@ extern "C" int ckpt_export_handle(ckpt_ctx *c, void *buf, uint64_t *len) {
     b.full_copy = c->full_copy;
     b.staging_bytes = c->staging_bytes;
     b.nonce = c->my_nonce;
+    b.arena_key = c->opt.arena_key;
+    b.attached_id = c->attached_id;
     gethostname(b.host, sizeof b.host - 1);
     CUDA_TRY(cudaIpcGetMemHandle(&b.staging_h, c->staging));
     CUDA_TRY(cudaIpcGetMemHandle(&b.flags_h, c->flags));
@@ -761,9 +842,60 @@ static int alloc_arena(ckpt_ctx *c) {
     if (device_only(c)) return CKPT_OK;  // the image lives in the device staging
     const uint64_t pbytes = parity_bytes_of(c);
     int rc = CKPT_OK;
+    // persistent arena: re-attach this member's files if their metadata matches the
+    // group's geometry, else start them fresh
+    const bool keyed = use_shm(c) && c->opt.arena_key;
+    bool reuse = false;
+    if (keyed) {
+        if (!c->meta) {
+            int r2 = shm_create(c->meta_buf, meta_name(c->opt.arena_key, c->me), 4096);
+            if (r2 == CKPT_OK) {
+                cudaHostUnregister(c->meta_buf.p);
+                c->meta_buf.registered = false;
+                c->meta_buf.kind = kShmPeer;  // persistent
+                c->meta = (ArenaMeta *)c->meta_buf.p;
+            } else {
+                return r2;
+            }
+        }
+        ArenaMeta *mt = c->meta;
+        reuse = mt->magic == kMetaMagic && mt->L == c->L && mt->Lstar == c->Lstar && mt->unit == c->unit &&
+                mt->m == c->m && mt->me == c->me && mt->scheme == c->scheme && mt->nbuf == (uint32_t)c->nbuf &&
+                mt->align == c->opt.align;
+        if (!reuse) {
+            __atomic_store_n(&mt->state, 0ull, __ATOMIC_RELEASE);
+            mt->magic = kMetaMagic;
+            mt->version = kAbiVersion;
+            mt->L = c->L;
+            mt->Lstar = c->Lstar;
+            mt->unit = c->unit;
+            mt->m = c->m;
+            mt->me = c->me;
+            mt->scheme = c->scheme;
+            mt->nbuf = (uint32_t)c->nbuf;
+            mt->align = c->opt.align;
+            for (int i = 0; i < c->nbuf; ++i) shm_unlink(shm_name(c->opt.arena_key, c->me, i).c_str());
+            c->attached_id = 0;
+            c->attached_idx = -1;
+        }
+    }
     for (int i = 0; i < c->nbuf && !rc; ++i) {
         if (use_shm(c)) {
-            rc = shm_create(c->shm_own[i], shm_name(c->group_nonce, c->me, i), shm_bytes(c));
+            const std::string nm = shm_name(c->group_nonce, c->me, i);
+            if (reuse) {
+                rc = shm_attach(c->shm_own[i], nm, shm_bytes(c), true);
+                if (rc == CKPT_ENOSNAP) {  // file gone (lost host memory): fresh
+                    reuse = false;
+                    c->attached_id = 0;
+                    c->attached_idx = -1;
+                    __atomic_store_n(&c->meta->state, 0ull, __ATOMIC_RELEASE);
+                    rc = CKPT_OK;
+                }
+            }
+            if (!c->shm_own[i].p) {
+                rc = shm_create(c->shm_own[i], nm, shm_bytes(c));
+                if (!rc && keyed) c->shm_own[i].kind = kShmPeer;  // persistent: never unlinked here
+            }
             if (rc) break;
             uint8_t *base = c->shm_own[i].p;
             c->hdata[i] = HostBuf{base, c->Lstar, kView, true, ""};
@@ -785,9 +917,26 @@ static int alloc_arena(ckpt_ctx *c) {
         }
         return rc;
     }
+    // snapshot id n lives in host buffer (n-1) % nbuf on every member: continue from the
+    // group's committed version (max over members' attached ids, 0 for a fresh group)
+    c->next_id = c->group_version + 1;
+    c->ongoing = (int)(c->group_version % (uint64_t)c->nbuf);
     c->completed = -1;
-    c->ongoing = 0;
+    c->completed_id = 0;
+    if (keyed && reuse && c->attached_id == c->group_version && c->attached_idx >= 0 &&
+        c->attached_idx == (int)((c->group_version - 1) % (uint64_t)c->nbuf)) {
+        c->completed = c->attached_idx;
+        c->completed_id = c->attached_id;
+    }
     return CKPT_OK;
+}
+
+// Publish the committed version in the persistent arena's metadata (one atomic store,
+// after every byte of the image is in host memory).
+static void meta_commit(ckpt_ctx *c) {
+    if (!c->meta) return;
+    const uint64_t st = c->completed < 0 ? 0 : (c->completed_id << 8) | (uint64_t)(c->completed + 1);
+    __atomic_store_n(&c->meta->state, st, __ATOMIC_RELEASE);
 }
 
 // ARC push targets: the files of my holder (member me-1), pinned so that my copy engine
@@ -818,7 +967,9 @@ static int ensure_next_mapped(ckpt_ctx *c) {
 static int setup_ungrouped(ckpt_ctx *c) {
     c->m = 1;
     c->me = 0;
-    c->group_nonce = c->my_nonce;
+    c->group_nonce = (use_shm(c) && c->opt.arena_key) ? c->opt.arena_key : c->my_nonce;
+    c->group_version = c->attached_id;
+    c->scheme = CKPT_SCHEME_AEC;
     c->arc = false;
     c->aec = true;
     c->Lstar = c->L;
@@ -871,6 +1022,12 @@ extern "C" int ckpt_protect(ckpt_ctx *c, const ckpt_group *g) {
         if (hb[g->my_index]->pid != (int32_t)getpid() || hb[g->my_index]->L != c->L)
             return fail(CKPT_EINVAL, "protect: my_index does not point at this context's handle");
         c->group_nonce = hb[0]->nonce;
+        c->group_version = 0;
+        for (uint32_t j = 0; j < m; ++j) {
+            if (hb[j]->arena_key != c->opt.arena_key)
+                return fail(CKPT_EMISMATCH, "protect: member %u uses another arena key", j);
+            c->group_version = std::max(c->group_version, hb[j]->attached_id);
+        }
         for (uint32_t j = 0; j < m; ++j) {
             c->peer_L[j] = Ls[j];
             if (j == g->my_index) {
@@ -903,6 +1060,13 @@ extern "C" int ckpt_protect(ckpt_ctx *c, const ckpt_group *g) {
         if (g->members[g->my_index] != c) return fail(CKPT_EINVAL, "protect: members[my_index] is not this context");
         if (!g->members[0]) return fail(CKPT_EINVAL, "protect: LOCAL group member 0 is NULL");
         c->group_nonce = g->members[0]->my_nonce;
+        c->group_version = 0;
+        for (uint32_t j = 0; j < m; ++j) {
+            if (!g->members[j]) return fail(CKPT_EINVAL, "protect: LOCAL group member %u is NULL", j);
+            if (g->members[j]->opt.arena_key != c->opt.arena_key)
+                return fail(CKPT_EMISMATCH, "protect: member %u uses another arena key", j);
+            c->group_version = std::max(c->group_version, g->members[j]->attached_id);
+        }
         for (uint32_t j = 0; j < m; ++j) {
             ckpt_ctx *o = g->members[j];
             if (!o || !o->registered) return fail(CKPT_ESTATE, "protect: member %u not registered", j);
@@ -941,6 +1105,12 @@ extern "C" int ckpt_protect(ckpt_ctx *c, const ckpt_group *g) {
     c->scheme = scheme;
     c->arc = arc;
     c->aec = scheme == CKPT_SCHEME_AEC || scheme == CKPT_SCHEME_ARC_AEC;
+    if (use_shm(c) && c->opt.arena_key) {
+        if (c->arena_member != c->me)
+            return fail(CKPT_EINVAL, "protect: persistent arena member %u (layout.local_rank) != group index %u",
+                        c->arena_member, c->me);
+        c->group_nonce = c->opt.arena_key;
+    }
     // parity buffer (local)
     if (!c->aec) {
         c->parity_bytes = 0;
@@ -1496,7 +1666,10 @@ static int stage_finish(ckpt_ctx *c) {
 static int begin_member(ckpt_ctx *c, cudaStream_t caller, uint64_t B) {
     int rc = prepare_op(c, B);
     if (rc) return rc;
-    if (c->nbuf == 1) c->completed = -1;  // single buffer: overwritten in place
+    if (c->nbuf == 1) {  // single buffer: overwritten in place
+        c->completed = -1;
+        meta_commit(c);
+    }
     CUDA_TRY(cudaEventRecord(c->ev_capture, caller));
     if (c->opt.flags & CKPT_OPT_TIMING) CUDA_TRY(cudaEventRecord(c->ev_t0, caller));
     CUDA_TRY(cudaStreamWaitEvent(c->sP, c->ev_capture, 0));
@@ -1532,7 +1705,10 @@ extern "C" int ckpt_snapshot(ckpt_ctx *c, uint64_t bucket_bytes, void *stream, u
             for (uint32_t j = 0; j < c->m; ++j) {
                 ckpt_ctx *o = c->members[j];
                 if ((rc = set_dev(o)) || (rc = prepare_op(o, B))) return rc;
-                if (o->nbuf == 1) o->completed = -1;
+                if (o->nbuf == 1) {
+                    o->completed = -1;
+                    meta_commit(o);
+                }
                 CUDA_TRY(cudaStreamWaitEvent(o->sP, o->ev_capture, 0));
                 if (o->opt.flags & CKPT_OPT_TIMING) CUDA_TRY(cudaEventRecord(o->ev_t0, o->sP));
             }
@@ -1686,6 +1862,7 @@ extern "C" int ckpt_wait(ckpt_ctx *c, uint64_t id) {
     c->completed = c->ongoing;
     c->completed_id = id;
     if (c->nbuf == 2) c->ongoing ^= 1;
+    meta_commit(c);
     return CKPT_OK;
 }
 
@@ -1823,6 +2000,7 @@ static int rb_commit(ckpt_ctx *c, uint32_t kl, uint64_t version) {
         clean_pad(c, rb_target(c));
         c->completed = rb_target(c);
         c->completed_id = version;
+        meta_commit(c);
     }
     c->st.rebuilds++;
     return CKPT_OK;
@@ -1949,6 +2127,7 @@ static int recover_step1(ckpt_ctx *c, uint32_t mask, uint64_t version) {
     c->pad_dirty[idx] = false;  // the holder's copy carries the image's zero pad
     c->completed = idx;
     c->completed_id = version;
+    meta_commit(c);
     c->st.h2d_bytes += 0;
     return CKPT_OK;
 }
@@ -2028,6 +2207,7 @@ extern "C" int ckpt_forget(ckpt_ctx *c, uint8_t poison) {
     }
     c->completed = -1;
     c->completed_id = 0;
+    meta_commit(c);
     return CKPT_OK;
 }
 
