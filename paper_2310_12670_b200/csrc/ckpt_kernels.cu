@@ -11,6 +11,7 @@
 //    for the encode: (m-1) peer units in per parity unit out.
 //
 // No tensor cores: the path is pure data movement.
+#include <algorithm>
 #include <cstdlib>
 
 #include "ckpt_kernels.cuh"
@@ -662,6 +663,12 @@ cudaError_t launch_pack(const PackArgs &a, int max_ctas, cudaStream_t s, bool tm
 
 cudaError_t launch_xor(const XorArgs &a, int max_ctas, cudaStream_t s) {
     if (a.nstripes == 0 || a.nin < 1 || a.nin > kMaxTerms || (a.unit & 15)) return cudaErrorInvalidValue;
+    static int mult = -1;  // CTAs per (pack) CTA budget: more warps hide NVLink latency
+    if (mult < 0) {
+        const char *e = getenv("CKPT_XOR_GRID_MULT");
+        mult = e ? std::max(1, atoi(e)) : 1;
+    }
+    max_ctas *= mult;
     switch (a.nin) {
         case 1: return launch_xor_n<1>(a, max_ctas, s);
         case 2: return launch_xor_n<2>(a, max_ctas, s);

@@ -36,10 +36,18 @@
 
 #include <random>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "../../include/ckpt.h"
 #include "ckpt_kernels.cuh"
 
 using namespace reft;
+
+// NVTX ranges around the public calls (host-side enqueue/wait), for nsys timelines.
+struct NvtxRange {
+    explicit NvtxRange(const char *name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+};
 
 // ------------------------------------------------------------------ errors ----------
 static thread_local std::string g_last_error;
@@ -1677,6 +1685,7 @@ static int begin_member(ckpt_ctx *c, cudaStream_t caller, uint64_t B) {
 }
 
 extern "C" int ckpt_snapshot(ckpt_ctx *c, uint64_t bucket_bytes, void *stream, uint64_t *id) {
+    NvtxRange nvtx_("ckpt_snapshot");
     if (!c) return fail(CKPT_EINVAL, "snapshot: null context");
     if (!c->registered) return fail(CKPT_ESTATE, "snapshot: not registered");
     int rc = check_sticky(c);
@@ -1838,6 +1847,7 @@ static int wait_done_all(ckpt_ctx *c, uint32_t done_seq) {
 }
 
 extern "C" int ckpt_wait(ckpt_ctx *c, uint64_t id) {
+    NvtxRange nvtx_("ckpt_wait");
     if (!c) return fail(CKPT_EINVAL, "wait: null");
     if (id == 0 || id >= c->next_id) return fail(CKPT_ESTATE, "wait: unknown snapshot id %llu", (unsigned long long)id);
     if (id != c->pending_id) return c->completed_id >= id ? CKPT_OK : fail(CKPT_ESTATE, "wait: snapshot %llu was not committed", (unsigned long long)id);
@@ -1868,6 +1878,7 @@ extern "C" int ckpt_wait(ckpt_ctx *c, uint64_t id) {
 
 // ------------------------------------------------------------------ load ------------
 extern "C" int ckpt_load(ckpt_ctx *c, void *stream) {
+    NvtxRange nvtx_("ckpt_load");
     if (!c) return fail(CKPT_EINVAL, "load: null");
     if (!c->registered) return fail(CKPT_ESTATE, "load: not registered");
     int rc = check_sticky(c);
@@ -2017,6 +2028,7 @@ extern "C" int ckpt_rebuild(ckpt_ctx *c, int32_t lost, void *stream) {
 }
 
 static int rebuild_aec(ckpt_ctx *c, int32_t lost, void *stream) {
+    NvtxRange nvtx_("ckpt_rebuild");
     if (!c) return fail(CKPT_EINVAL, "rebuild: null");
     if (!c->registered || !c->grouped) return fail(CKPT_ESTATE, "rebuild: not protected");
     if (c->m < 2) return fail(CKPT_EUNRECOVERABLE, "rebuild: a group of one has no redundancy (P.460)");
@@ -2146,6 +2158,7 @@ static int recover_step3(ckpt_ctx *c, uint32_t mask) {
 }
 
 extern "C" int ckpt_recover(ckpt_ctx *c, uint32_t mask, void *stream) {
+    NvtxRange nvtx_("ckpt_recover");
     if (!c) return fail(CKPT_EINVAL, "recover: null");
     if (!c->registered || !c->grouped) return fail(CKPT_ESTATE, "recover: not protected");
     if (c->m < 2) return fail(CKPT_EUNRECOVERABLE, "recover: a group of one has no redundancy (P.460)");

@@ -34,6 +34,7 @@ def main():
     p.add_argument("--lost", default="")
     p.add_argument("--scheme", type=int, default=0, help="CKPT_SCHEME_*: 1 AEC, 2 ARC, 3 ARC+AEC")
     p.add_argument("--host-buffers", type=int, default=2)
+    p.add_argument("--corun", action="store_true", help="bf16 GEMM co-run slowdown per bucket size (bench.py's)")
     a = p.parse_args()
     import torch
     import torch.distributed as dist
@@ -98,6 +99,11 @@ def main():
                "pack_hbm_gbs": round(st["pack_bytes"] / max(st["pack_ms"], 1e-9) / 1e6, 1),
                "xor_nvlink_gbs": round(st["xor_bytes_in"] / max(st["xor_ms"], 1e-9) / 1e6, 1),
                "launches_per_snapshot": (st["pack_launches"] + st["xor_launches"]) // a.reps}
+        if a.corun:
+            import bench
+            co = bench.gemm_corun(torch, C, ctx, st0, bmib << 20, bar, amax, dev)
+            rec["gemm_slowdown_pct"] = co["slowdown_pct"]
+            rec["snapshot_ms_while_corunning"] = co["snapshot_ms_while_corunning"]
         if a.drill and g["m"] >= 2:
             lost = [tuple(int(y) for y in x.split("+")) for x in a.lost.split(",")] if a.lost else [(0,), (g["m"] - 1,)]
             C.ckpt_stats_reset(ctx)
