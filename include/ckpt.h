@@ -72,6 +72,9 @@ extern "C" {
                                       D2H, no host arena; load/rebuild work from HBM.  A
                                       single device image: a failed snapshot destroys the
                                       previous one.  Measures the device-side protect path. */
+#define CKPT_OPT_HOST_LOAD   0x80u /* always restore (load / rebuild sources) from the host
+                                      image, never from a still-valid device copy (the
+                                      paper's REFT-load after a full restart, P.545)       */
 #define CKPT_OPT_SHM_ARENA   0x40u /* host arena in POSIX shared memory (/dev/shm), one file
                                       per member and host buffer: peers (ARC) and a restarted
                                       process can reach it; required by the ARC schemes     */
@@ -249,7 +252,10 @@ int ckpt_wait(ckpt_ctx *ctx, uint64_t id);
 
 /* Restore every registered tensor from the last COMPLETED image (H2D + unpack),
  * ordered on `stream`; returns after enqueueing (stream-ordered, host-async).
- * Local only: no communication.  Errors: ENOSNAP, ESTATE, ECUDA. */
+ * Local only: no communication.  With full-copy staging the library's device copy of
+ * the completed image is used directly (no H2D) while it is still valid -- from the
+ * commit until the next snapshot starts packing, unless ckpt_forget declared the device
+ * lost; CKPT_OPT_HOST_LOAD forces the host path.  Errors: ENOSNAP, ESTATE, ECUDA. */
 int ckpt_load(ckpt_ctx *ctx, void *stream);
 
 /* Rebuild lost member `lost_rank`'s completed image (data and its parity row) from

@@ -223,6 +223,8 @@ struct ckpt_ctx {
     int completed = -1, ongoing = 0;
     bool pad_dirty[2] = {false, false};  // zero pad [L, L*) overwritten by ckpt_forget
     uint64_t completed_id = 0;
+    uint64_t staging_id = 0;  // id of the image the device staging + parity hold (0: none)
+    bool staging_poisoned = false;  // ckpt_forget wrote over the staging's zero gaps
 
     // streams / events
     cudaStream_t sP = nullptr, sX = nullptr, sC = nullptr, sW = nullptr, sG = nullptr;
@@ -837,6 +839,15 @@ extern "C" int ckpt_export_handle(ckpt_ctx *c, void *buf, uint64_t *len) {
 
 static inline bool device_only(const ckpt_ctx *c) { return (c->opt.flags & CKPT_OPT_DEVICE_ONLY) != 0; }
 
+// The device staging (and parity buffer) still hold the completed image: true in
+// DEVICE_ONLY mode, and with full-copy staging from a commit until the next snapshot
+// packs over it (or ckpt_forget declares the device lost).
+static inline bool device_image_valid(const ckpt_ctx *c) {
+    if (device_only(c)) return true;
+    return c->full_copy && !(c->opt.flags & CKPT_OPT_HOST_LOAD) && c->staging_id != 0 &&
+           c->staging_id == c->completed_id && c->completed >= 0;
+}
+
 static inline uint64_t parity_bytes_of(const ckpt_ctx *c) { return c->m >= 2 && c->aec ? c->Lstar / (c->m - 1) : 0; }
 static inline uint64_t shm_bytes(const ckpt_ctx *c) {
     const uint64_t P = parity_bytes_of(c);
@@ -1241,7 +1252,7 @@ static int do_pack_ce(ckpt_ctx *c, uint64_t k, uint8_t *slot, cudaStream_t s, bo
     const uint64_t bb = bucket_begin(c, k), be = std::min(bucket_end(c, k), c->L);
     const uint64_t t_lo = bb / kTile, t_hi = (be + kTile - 1) / kTile;
     uint64_t ci = c->tile_first[t_lo], ce = c->tile_first[t_hi];
-    if (!unpack && !c->full_copy) {
+    if (!unpack && (!c->full_copy || c->staging_poisoned)) {
         CUDA_TRY(cudaMemsetAsync(slot, 0, be - bb, s));
         c->st.ce_copies++;
     }
@@ -1259,10 +1270,7 @@ static int do_pack_ce(ckpt_ctx *c, uint64_t k, uint8_t *slot, cudaStream_t s, bo
         CUDA_TRY(cudaMemcpyAsync(unpack ? tensor : sl, unpack ? sl : tensor, hi - lo, cudaMemcpyDeviceToDevice, s));
         c->st.ce_copies++;
     }
-    if (unpack)
-        c->st.unpack_launches += 0;
-    else
-        c->st.pack_bytes += 2 * (be - bb);
+    if (!unpack) c->st.pack_bytes += 2 * (be - bb);  // CE pieces are counted in ce_copies
     return CKPT_OK;
 }
 
@@ -1674,6 +1682,7 @@ static int stage_finish(ckpt_ctx *c) {
 static int begin_member(ckpt_ctx *c, cudaStream_t caller, uint64_t B) {
     int rc = prepare_op(c, B);
     if (rc) return rc;
+    c->staging_id = 0;  // the pack overwrites the device copy
     if (c->nbuf == 1) {  // single buffer: overwritten in place
         c->completed = -1;
         meta_commit(c);
@@ -1714,6 +1723,7 @@ extern "C" int ckpt_snapshot(ckpt_ctx *c, uint64_t bucket_bytes, void *stream, u
             for (uint32_t j = 0; j < c->m; ++j) {
                 ckpt_ctx *o = c->members[j];
                 if ((rc = set_dev(o)) || (rc = prepare_op(o, B))) return rc;
+                o->staging_id = 0;
                 if (o->nbuf == 1) {
                     o->completed = -1;
                     meta_commit(o);
@@ -1872,6 +1882,8 @@ extern "C" int ckpt_wait(ckpt_ctx *c, uint64_t id) {
     c->completed = c->ongoing;
     c->completed_id = id;
     if (c->nbuf == 2) c->ongoing ^= 1;
+    if (c->full_copy) c->staging_id = id;
+    c->staging_poisoned = false;
     meta_commit(c);
     return CKPT_OK;
 }
@@ -1894,14 +1906,15 @@ extern "C" int ckpt_load(ckpt_ctx *c, void *stream) {
     c->seq = saved_seq;  // local op: no group sequence numbers consumed
     CUDA_TRY(cudaEventRecord(c->ev_capture, caller));
     CUDA_TRY(cudaStreamWaitEvent(c->sC, c->ev_capture, 0));
-    const uint8_t *img = device_only(c) ? nullptr : c->hdata[c->completed].p;
+    const bool from_dev = device_image_valid(c);
+    const uint8_t *img = from_dev ? nullptr : c->hdata[c->completed].p;
     for (uint64_t k = 0; k < c->op_NB; ++k) {
         const uint32_t s = slot_of(c, k);
         const uint64_t bb = bucket_begin(c, k);
         const uint64_t v = valid_in_bucket(c->L, bb, bucket_end(c, k));
         if (!v) continue;
         if (ring_reuse(c, k)) CUDA_TRY(cudaStreamWaitEvent(c->sC, c->ev_kdone[s], 0));
-        if (!device_only(c)) {
+        if (!from_dev) {
             CUDA_TRY(cudaMemcpyAsync(slot_ptr(c, c->staging, k), img + bb, v, cudaMemcpyHostToDevice, c->sC));
             c->st.h2d_bytes += v;
         }
@@ -1914,6 +1927,8 @@ extern "C" int ckpt_load(ckpt_ctx *c, void *stream) {
     CUDA_TRY(cudaEventRecord(c->ev_pack_all, c->sP));
     CUDA_TRY(cudaStreamWaitEvent(caller, c->ev_pack_all, 0));
     c->st.loads++;
+    // a host-path load over full-copy staging leaves the data image there (its parity
+    // buffer is not reloaded, so it is not a complete device image for a rebuild)
     if (c->opt.flags & CKPT_OPT_TIMING) {
         CUDA_TRY(cudaStreamSynchronize(c->sP));
         rc = harvest_timing(c);
@@ -1938,7 +1953,7 @@ static int rb_stage1(ckpt_ctx *c, uint64_t b, uint32_t kl) {
         }
         const uint64_t v = valid_in_bucket(c->L, bb, be);
         const uint64_t pb = (be - bb) / (c->m - 1);
-        if (!device_only(c)) {  // device-only: staging and parity already hold the image
+        if (!device_image_valid(c)) {  // else staging and parity already hold the image
             if (v) CUDA_TRY(cudaMemcpyAsync(slot_ptr(c, c->staging, b), c->hdata[c->completed].p + bb, v, cudaMemcpyHostToDevice, c->sC));
             CUDA_TRY(cudaMemcpyAsync(parity_slot_ptr(c, b), c->hpar[c->completed].p + bb / (c->m - 1), pb, cudaMemcpyHostToDevice, c->sC));
             c->st.h2d_bytes += v + pb;
@@ -2013,6 +2028,9 @@ static int rb_commit(ckpt_ctx *c, uint32_t kl, uint64_t version) {
         c->completed_id = version;
         meta_commit(c);
     }
+    // full-copy staging now holds every member's completed image (survivors staged or
+    // kept theirs, the lost member's was rebuilt and re-encoded in place)
+    if (c->full_copy) c->staging_id = c->completed_id;
     c->st.rebuilds++;
     return CKPT_OK;
 }
@@ -2140,7 +2158,6 @@ static int recover_step1(ckpt_ctx *c, uint32_t mask, uint64_t version) {
     c->completed = idx;
     c->completed_id = version;
     meta_commit(c);
-    c->st.h2d_bytes += 0;
     return CKPT_OK;
 }
 
@@ -2201,7 +2218,9 @@ extern "C" int ckpt_recover(ckpt_ctx *c, uint32_t mask, void *stream) {
 extern "C" int ckpt_forget(ckpt_ctx *c, uint8_t poison) {
     if (!c) return fail(CKPT_EINVAL, "forget: null");
     if (c->pending_id || c->requested) return fail(CKPT_ESTATE, "forget: a snapshot is in flight");
-    if (device_only(c) && c->staging) {  // the image is in HBM: poison staging + parity
+    c->staging_id = 0;
+    c->staging_poisoned = true;
+    if (c->staging) {  // the device copy is lost with the member: poison staging + parity
         int rc = set_dev(c);
         if (rc) return rc;
         CUDA_TRY(cudaMemset(c->staging, poison, c->staging_bytes));

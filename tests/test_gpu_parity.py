@@ -155,7 +155,8 @@ def test_group_encode_matches_oracle(torch, C, m, unit, n_slots, bucket, flags):
 
 @pytest.mark.parametrize("m,unit,n_slots,flags", [(2, 4096, 0, 0), (3, 4096, 2, 0), (4, 65536, 0, 0x2),
                                                   (8, 1024, 3, 0), (8, 0, 0, 0), (5, 64, 2, 0x2),
-                                                  (4, 4096, 2, 0x18), (6, 256, 0, 0x18)])
+                                                  (4, 4096, 2, 0x18), (6, 256, 0, 0x18),
+                                                  (4, 65536, 0, 0x80), (3, 4096, 0, 0x82), (5, 4096, 0, 0x88)])
 def test_group_drill_rebuild_every_rank(torch, C, m, unit, n_slots, flags):
     """Failure drill (Q12): rank k loses tensors and host image; rebuild + load."""
     from synth.gpu import fill_state
@@ -536,3 +537,32 @@ def test_shm_arena_aec_matches_anon(torch, C):
     finally:
         for c in ctxs:
             C.ckpt_destroy(c)
+
+
+def test_load_from_device_copy_and_host_path_agree(torch, C):
+    """With full-copy staging, ckpt_load right after a commit restores from the device copy
+    (no H2D); CKPT_OPT_HOST_LOAD restores from host memory -- same bytes, and the stats
+    show which path ran."""
+    from synth.gpu import fill_state
+    for flags, expect_h2d in ((0, False), (0x80, True)):
+        st = tiny(0, n=9, misalign=1)
+        specs, ts = st
+        ctx = make_ctx(C, st, n_slots=0, bucket_bytes=1 << 16, flags=flags)
+        try:
+            C.ckpt_protect(ctx, 1, 0)
+            sid = C.ckpt_snapshot(ctx)
+            C.ckpt_wait(ctx, sid)
+            fill_state(ts, 0, seed=77, xor_mode=1)
+            C.ckpt_stats_reset(ctx)
+            C.ckpt_load(ctx)
+            torch.cuda.synchronize()
+            assert (C.ckpt_get_stats(ctx)["h2d_bytes"] > 0) == expect_h2d
+            for t, (x, w) in enumerate(zip(ts, oracle_tensor_bytes(specs, 0))):
+                assert_bytes_equal(tensor_bytes(x), w, f"flags={flags:#x} tensor {t}")
+            # a snapshot in flight invalidates the device copy: load must refuse
+            sid = C.ckpt_snapshot(ctx)
+            with pytest.raises(C.CkptError):
+                C.ckpt_load(ctx)
+            C.ckpt_wait(ctx, sid)
+        finally:
+            C.ckpt_destroy(ctx)

@@ -96,8 +96,9 @@ def main():
                "state_gbs_per_gpu": round(S / t / 1e9, 3), "wire_gbs_per_gpu": round(st["d2h_bytes"] / a.reps / t / 1e9, 3),
                "pack_us_per_launch": round(st["pack_ms"] / max(st["pack_launches"], 1) * 1e3, 2),
                "xor_us_per_launch": round(st["xor_ms"] / max(st["xor_launches"], 1) * 1e3, 2),
-               "pack_hbm_gbs": round(st["pack_bytes"] / max(st["pack_ms"], 1e-9) / 1e6, 1),
-               "xor_nvlink_gbs": round(st["xor_bytes_in"] / max(st["xor_ms"], 1e-9) / 1e6, 1),
+               "pack_hbm_gbs": round(st["pack_bytes"] / st["pack_ms"] / 1e6, 1) if st["pack_ms"] > 0 else None,
+               "xor_nvlink_gbs": round(st["xor_bytes_in"] / st["xor_ms"] / 1e6, 1)
+               if st["xor_ms"] > 0 and not (a.flags & C.CKPT_OPT_CE_GATHER) else None,
                "launches_per_snapshot": (st["pack_launches"] + st["xor_launches"]) // a.reps}
         if a.corun:
             import bench
