@@ -281,6 +281,13 @@ int ckpt_rebuild(ckpt_ctx *ctx, int32_t lost_rank, void *stream);
  * ECUDA, EPEER. */
 int ckpt_recover(ckpt_ctx *ctx, uint32_t lost_mask, void *stream);
 
+/* Host-block until every asynchronous host-image write of this context is complete:
+ * after ckpt_rebuild with full-copy staging the lost member's call returns once its
+ * DEVICE image is rebuilt (ckpt_load can run at once) while its host image is re-written
+ * in the background; the next snapshot, ckpt_load from host, ckpt_host_view and
+ * ckpt_forget wait for it implicitly. */
+int ckpt_sync(ckpt_ctx *ctx);
+
 /* Failure injection for drills (Q12, hardware-loss semantics): overwrite this
  * member's completed and ongoing host images with `poison` and mark it as having no
  * completed snapshot (it can only be restored by ckpt_rebuild). */

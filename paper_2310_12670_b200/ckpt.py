@@ -117,6 +117,7 @@ def lib():
             "ckpt_load": (ctypes.c_int, [_vp, _vp]),
             "ckpt_rebuild": (ctypes.c_int, [_vp, _i32, _vp]),
             "ckpt_recover": (ctypes.c_int, [_vp, _u32, _vp]),
+            "ckpt_sync": (ctypes.c_int, [_vp]),
             "ckpt_forget": (ctypes.c_int, [_vp, ctypes.c_uint8]),
             "ckpt_host_view": (ctypes.c_int, [_vp, ctypes.c_int, ctypes.POINTER(_vp), ctypes.POINTER(_u64),
                                               ctypes.POINTER(_vp), ctypes.POINTER(_u64)]),
@@ -270,6 +271,10 @@ def ckpt_rebuild(ctx: int, lost_rank: int, stream=None) -> None:
 
 def ckpt_recover(ctx: int, lost_mask: int, stream=None) -> None:
     _check(lib().ckpt_recover(ctx, lost_mask, _stream_handle(stream)), "ckpt_recover")
+
+
+def ckpt_sync(ctx: int) -> None:
+    _check(lib().ckpt_sync(ctx), "ckpt_sync")
 
 
 def ckpt_forget(ctx: int, poison: int = 0xA5) -> None:

@@ -225,6 +225,7 @@ struct ckpt_ctx {
     uint64_t completed_id = 0;
     uint64_t staging_id = 0;  // id of the image the device staging + parity hold (0: none)
     bool staging_poisoned = false;  // ckpt_forget wrote over the staging's zero gaps
+    bool host_pending = false;      // a rebuilt image is still being copied to host (ev_done)
 
     // streams / events
     cudaStream_t sP = nullptr, sX = nullptr, sC = nullptr, sW = nullptr, sG = nullptr;
@@ -1408,6 +1409,8 @@ static void make_sticky(ckpt_ctx *c, int rc) {
 // Bucket = whole stripes ((m-1)u; A when unprotected).  With full-copy staging the
 // single-launch pack also needs whole 64 KiB tile groups: B is rounded down to a
 // multiple of lcm(stripe, kGroup).
+static int host_sync(ckpt_ctx *c);
+
 static uint64_t effective_bucket(const ckpt_ctx *c, uint64_t req) {
     uint64_t B = req ? req : c->opt.bucket_bytes;
     uint64_t q = c->m >= 2 ? (uint64_t)(c->m - 1) * c->unit : (uint64_t)c->opt.align;
@@ -1699,6 +1702,7 @@ extern "C" int ckpt_snapshot(ckpt_ctx *c, uint64_t bucket_bytes, void *stream, u
     if (!c->registered) return fail(CKPT_ESTATE, "snapshot: not registered");
     int rc = check_sticky(c);
     if (rc) return rc;
+    if ((rc = host_sync(c))) return rc;  // the pack must not overwrite a staging still being copied
     if (c->pending_id || c->requested) return fail(CKPT_EBUSY, "snapshot: previous snapshot %llu not waited", (unsigned long long)c->pending_id);
     if ((rc = set_dev(c))) return rc;
     if (!c->grouped && (rc = setup_ungrouped(c))) return rc;
@@ -1898,6 +1902,7 @@ extern "C" int ckpt_load(ckpt_ctx *c, void *stream) {
     if (c->pending_id || c->requested) return fail(CKPT_ESTATE, "load: a snapshot is in flight");
     if (c->rebuild_requested) return fail(CKPT_ESTATE, "load: a LOCAL group rebuild is not complete");
     if (!c->grouped || c->completed < 0) return fail(CKPT_ENOSNAP, "load: no completed snapshot");
+    if (!device_image_valid(c) && (rc = host_sync(c))) return rc;
     if ((rc = set_dev(c))) return rc;
     cudaStream_t caller = (cudaStream_t)stream;
     // op geometry: bucket = ring slot (or the default bucket in full-copy mode)
@@ -1987,12 +1992,24 @@ static int rb_stage2(ckpt_ctx *c, uint64_t b, uint32_t kl) {
 // `ongoing` in step with the group (ARC pushes rely on identical indices).
 static inline int rb_target(const ckpt_ctx *c) { return c->nbuf == 2 ? c->ongoing ^ 1 : 0; }
 
+// Background host restore: with full-copy staging (and no ARC copies to re-create from
+// it) the lost member's rebuild returns as soon as its DEVICE image is complete -- the
+// REL waits sit on the kernel stream, DONE is signalled from there -- while the D2H that
+// re-protects its host image keeps running on the copy stream (host_sync waits for it).
+static inline bool async_host_restore(const ckpt_ctx *c) { return c->full_copy && !device_only(c) && !c->arc; }
+
 static int rb_stage3(ckpt_ctx *c, uint64_t b, uint32_t kl) {
     if (c->me != kl) return CKPT_OK;
     const uint32_t s = slot_of(c, b);
     const uint64_t bb = bucket_begin(c, b), be = bucket_end(c, b);
     int rc;
-    if ((rc = wait_all(c, c->sC, kRel, bucket_seq(c, b), s))) return rc;
+    if (async_host_restore(c)) {
+        if ((rc = wait_all(c, c->sX, kRel, bucket_seq(c, b), s))) return rc;
+        CUDA_TRY(cudaEventRecord(c->ev_h2d[s], c->sX));  // bucket b of the device image complete
+        CUDA_TRY(cudaStreamWaitEvent(c->sC, c->ev_h2d[s], 0));
+    } else {
+        if ((rc = wait_all(c, c->sC, kRel, bucket_seq(c, b), s))) return rc;
+    }
     CUDA_TRY(cudaStreamWaitEvent(c->sC, c->ev_kdone[s], 0));
     const uint64_t v = valid_in_bucket(c->L, bb, be);
     const uint64_t pb = (be - bb) / (c->m - 1);
@@ -2007,26 +2024,59 @@ static int rb_stage3(ckpt_ctx *c, uint64_t b, uint32_t kl) {
     return CKPT_OK;
 }
 
-static int rb_finish(ckpt_ctx *c) {
-    // DONE after every local stream finished (the lost member's D2H is the last step)
+static int rb_finish(ckpt_ctx *c, uint32_t kl) {
     CUDA_TRY(cudaEventRecord(c->ev_pack_all, c->sX));
     CUDA_TRY(cudaStreamWaitEvent(c->sC, c->ev_pack_all, 0));
     CUDA_TRY(cudaEventRecord(c->ev_done, c->sC));
+    if (c->me == kl && async_host_restore(c))  // DONE = device image complete, D2H continues
+        return sig_signal(c, c->sX, kDone, c->op_seq_base + (uint32_t)c->op_NB + 1, 0);
+    // DONE after every local stream finished
     return sig_signal(c, c->sC, kDone, c->op_seq_base + (uint32_t)c->op_NB + 1, 0);
 }
 
+// Wait for a background host restore (see async_host_restore) and publish it.
+static int host_sync(ckpt_ctx *c) {
+    if (!c->host_pending) return CKPT_OK;
+    int rc = set_dev(c);
+    if (rc) return rc;
+    CUDA_TRY(cudaEventSynchronize(c->ev_done));
+    c->host_pending = false;
+    meta_commit(c);
+    return CKPT_OK;
+}
+
+extern "C" int ckpt_sync(ckpt_ctx *c) {
+    if (!c) return fail(CKPT_EINVAL, "sync: null");
+    return host_sync(c);
+}
+
 static int rb_commit(ckpt_ctx *c, uint32_t kl, uint64_t version) {
-    int rc = wait_done_all(c, c->op_seq_base + (uint32_t)c->op_NB + 1);
+    int rc;
+    const bool bg = c->me == kl && async_host_restore(c);
+    if (bg) {  // device image complete on sX; the copy stream is left running
+        if (!(rc = sync_stream_timeout(c, c->sP, "rebuild")) && !(rc = sync_stream_timeout(c, c->sX, "rebuild")) &&
+            c->transport == CKPT_GROUP_IPC && !(rc = wait_all(c, c->sW, kDone, c->op_seq_base + (uint32_t)c->op_NB + 1, 0)))
+            rc = sync_stream_timeout(c, c->sW, "rebuild(peers)");
+        if (!rc && c->transport == CKPT_GROUP_LOCAL)
+            for (uint32_t j = 0; j < c->m && !rc; ++j)
+                if (c->members[j] != c && cudaEventSynchronize(c->members[j]->ev_done) != cudaSuccess)
+                    rc = fail(CKPT_ECUDA, "rebuild: peer event");
+    } else {
+        rc = wait_done_all(c, c->op_seq_base + (uint32_t)c->op_NB + 1);
+    }
     if (!rc && (c->opt.flags & CKPT_OPT_TIMING)) rc = harvest_timing(c);
     if (rc) {
         make_sticky(c, rc);
         return rc;
     }
     if (c->me == kl) {
-        clean_pad(c, rb_target(c));
+        clean_pad(c, rb_target(c));  // the pad is disjoint from the D2H'd [0, L)
         c->completed = rb_target(c);
         c->completed_id = version;
-        meta_commit(c);
+        if (bg)
+            c->host_pending = true;  // meta is published by host_sync
+        else
+            meta_commit(c);
     }
     // full-copy staging now holds every member's completed image (survivors staged or
     // kept theirs, the lost member's was rebuilt and re-encoded in place)
@@ -2048,6 +2098,7 @@ extern "C" int ckpt_rebuild(ckpt_ctx *c, int32_t lost, void *stream) {
 static int rebuild_aec(ckpt_ctx *c, int32_t lost, void *stream) {
     NvtxRange nvtx_("ckpt_rebuild");
     if (!c) return fail(CKPT_EINVAL, "rebuild: null");
+    if (host_sync(c)) return CKPT_ECUDA;
     if (!c->registered || !c->grouped) return fail(CKPT_ESTATE, "rebuild: not protected");
     if (c->m < 2) return fail(CKPT_EUNRECOVERABLE, "rebuild: a group of one has no redundancy (P.460)");
     if (lost < 0 || (uint32_t)lost >= c->m) return fail(CKPT_EINVAL, "rebuild: lost rank %d out of range", lost);
@@ -2091,7 +2142,7 @@ static int rebuild_aec(ckpt_ctx *c, int32_t lost, void *stream) {
                 if ((rc = set_dev(c->members[j])) || (rc = rb_stage3(c->members[j], b, kl))) goto bad;
         }
         for (uint32_t j = 0; j < c->m; ++j)
-            if ((rc = set_dev(c->members[j])) || (rc = rb_finish(c->members[j]))) goto bad;
+            if ((rc = set_dev(c->members[j])) || (rc = rb_finish(c->members[j], kl))) goto bad;
         for (uint32_t j = 0; j < c->m; ++j) {
             ckpt_ctx *o = c->members[j];
             if ((rc = set_dev(o)) || (rc = rb_commit(o, kl, version))) goto bad;
@@ -2116,7 +2167,7 @@ static int rebuild_aec(ckpt_ctx *c, int32_t lost, void *stream) {
             return rc;
         }
     }
-    if ((rc = rb_finish(c))) {
+    if ((rc = rb_finish(c, kl))) {
         make_sticky(c, rc);
         return rc;
     }
@@ -2217,6 +2268,7 @@ extern "C" int ckpt_recover(ckpt_ctx *c, uint32_t mask, void *stream) {
 // ------------------------------------------------------------------ misc ------------
 extern "C" int ckpt_forget(ckpt_ctx *c, uint8_t poison) {
     if (!c) return fail(CKPT_EINVAL, "forget: null");
+    host_sync(c);
     if (c->pending_id || c->requested) return fail(CKPT_ESTATE, "forget: a snapshot is in flight");
     c->staging_id = 0;
     c->staging_poisoned = true;
@@ -2257,6 +2309,7 @@ extern "C" int ckpt_host_view(const ckpt_ctx *c, int which, const void **data, u
         return CKPT_OK;
     }
     if (!c->grouped) return fail(CKPT_ENOSNAP, "host_view: no host arena yet");
+    if (host_sync(const_cast<ckpt_ctx *>(c))) return CKPT_ECUDA;
     if (device_only(c)) return fail(CKPT_EINVAL, "host_view: DEVICE_ONLY context has no host image");
     int idx = which == 0 ? c->completed : c->ongoing;
     if (idx < 0) return fail(CKPT_ENOSNAP, "host_view: no completed snapshot");
