@@ -2203,9 +2203,12 @@ static int recover_step1(ckpt_ctx *c, uint32_t mask, uint64_t version) {
     if (rc) return rc;
     const int idx = rb_target(c);
     const uint64_t P = parity_bytes_of(c);
-    parallel_memcpy(c->hdata[idx].p, c->shm_hold[idx].p + c->Lstar + P, c->Lstar);
+    // only [0, L) carries data; the zero pad is written here, never copied (a peer's pad
+    // may still hold ckpt_forget poison while it is being cleaned)
+    parallel_memcpy(c->hdata[idx].p, c->shm_hold[idx].p + c->Lstar + P, c->L);
+    if (c->Lstar > c->L) memset(c->hdata[idx].p + c->L, 0, c->Lstar - c->L);
     if (c->aec) parallel_memcpy(c->hpar[idx].p, c->shm_hold[idx].p + 2 * c->Lstar + P, P);
-    c->pad_dirty[idx] = false;  // the holder's copy carries the image's zero pad
+    c->pad_dirty[idx] = false;
     c->completed = idx;
     c->completed_id = version;
     meta_commit(c);
@@ -2219,7 +2222,9 @@ static int recover_step3(ckpt_ctx *c, uint32_t mask) {
     const int idx = c->completed;
     if (idx < 0) return fail(CKPT_ESTATE, "recover: member %u has no completed image after restore", c->me);
     const uint64_t P = parity_bytes_of(c);
-    parallel_memcpy(c->harc[idx], c->shm_next[idx].p, c->Lstar);  // member me+1's data + pad
+    const uint64_t Ln = c->peer_L[(c->me + 1) % c->m];
+    parallel_memcpy(c->harc[idx], c->shm_next[idx].p, Ln);  // member me+1's data ...
+    if (c->Lstar > Ln) memset(c->harc[idx] + Ln, 0, c->Lstar - Ln);  // ... and a clean pad
     if (c->aec) parallel_memcpy(c->harcp[idx], c->shm_next[idx].p + c->Lstar, P);
     c->arc_dirty[idx] = false;
     return CKPT_OK;

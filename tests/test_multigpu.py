@@ -225,7 +225,7 @@ def test_ipc_full_size_sampled(config):
             if p.is_alive():
                 p.kill()
     for rank, ok, _ in res:
-        assert all(ok), (rank, ok)
+        assert all(ok), (rank, "failed checks (case index)", [i for i, x in enumerate(ok) if not x])
 
 
 def _worker_arc(rank, world, port, q, scheme):
@@ -336,4 +336,4 @@ def test_ipc_arc_schemes(scheme):
             if p.is_alive():
                 p.kill()
     for rank, ok, _ in res:
-        assert all(ok), (rank, ok)
+        assert all(ok), (rank, "failed checks (case index)", [i for i, x in enumerate(ok) if not x])

@@ -120,10 +120,12 @@ def main():
                 t0 = time.perf_counter()
                 C.ckpt_recover(ctx, mask)
                 t1 = time.perf_counter()
-                C.ckpt_load(ctx)
-                torch.cuda.synchronize()
+                C.ckpt_load(ctx, st0)
+                st0.synchronize()  # the training stream is ready (a background host restore may continue)
                 t2 = time.perf_counter()
-                rb, ld = amax(t1 - t0), amax(t2 - t1)
+                C.ckpt_sync(ctx)
+                t3 = time.perf_counter()
+                rb, ld, hs = amax(t1 - t0), amax(t2 - t1), amax(t3 - t0)
                 srb = C.ckpt_get_stats(ctx)
                 # bit-exact: every tensor of every rank equals the generator (sampled bytes)
                 ok = True
@@ -137,6 +139,7 @@ def main():
                 # bytes stored into the lost rank over NVLink, / mean launch time
                 kgbs = (srb["rebuild_bytes_in"] + srb["rebuild_bytes_out"]) / max(srb["rebuild_ms"], 1e-9) / 1e6
                 rec.setdefault("drill", []).append({"lost": k, "rebuild_ms": round(rb * 1e3, 2), "load_ms": round(ld * 1e3, 2),
+                                                    "host_reprotected_ms": round(hs * 1e3, 2),
                                                     "bit_exact_sampled": okall,
                                                     "rank0_rebuild_kernel_gbs": round(kgbs, 1) if rank not in k else None,
                                                     "rank0_rebuild_launches": srb["rebuild_launches"]})
