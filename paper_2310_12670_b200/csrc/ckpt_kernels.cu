@@ -632,6 +632,25 @@ cudaError_t launch_pack_all(const PackAllArgs &a, int max_ctas, cudaStream_t s, 
     return cudaGetLastError();
 }
 
+// CUDA lazy loading would load each kernel at its first launch, and loading can wait for
+// work in flight on the device (e.g. a background D2H); load them all up front instead.
+cudaError_t preload_kernels() {
+    cudaFuncAttributes fa;
+    const void *fns[] = {
+        (const void *)pack_kernel, (const void *)pack_all_kernel, (const void *)pack_tma_kernel,
+        (const void *)pack_all_tma_kernel<4>, (const void *)pack_all_tma_kernel<6>, (const void *)pack_all_tma_kernel<8>,
+        (const void *)xor_kernel<1, xor_unroll<1>()>, (const void *)xor_kernel<2, xor_unroll<2>()>,
+        (const void *)xor_kernel<3, xor_unroll<3>()>, (const void *)xor_kernel<4, xor_unroll<4>()>,
+        (const void *)xor_kernel<5, xor_unroll<5>()>, (const void *)xor_kernel<6, xor_unroll<6>()>,
+        (const void *)xor_kernel<7, xor_unroll<7>()>, (const void *)xor_kernel<8, xor_unroll<8>()>,
+        (const void *)signal_kernel};
+    for (const void *f : fns) {
+        cudaError_t e = cudaFuncGetAttributes(&fa, f);
+        if (e != cudaSuccess) return e;
+    }
+    return cudaSuccess;
+}
+
 cudaError_t launch_signal(const SignalArgs &a, cudaStream_t s) {
     signal_kernel<<<1, 32, 0, s>>>(a);
     return cudaGetLastError();

@@ -93,6 +93,7 @@ struct SignalArgs {
 
 // Launchers (return the cudaError_t of the launch).
 cudaError_t launch_signal(const SignalArgs &a, cudaStream_t s);
+cudaError_t preload_kernels();
 cudaError_t launch_pack_all(const PackAllArgs &a, int max_ctas, cudaStream_t s, bool tma);
 cudaError_t launch_pack(const PackArgs &a, int max_ctas, cudaStream_t s, bool tma);
 cudaError_t launch_xor(const XorArgs &a, int max_ctas, cudaStream_t s);

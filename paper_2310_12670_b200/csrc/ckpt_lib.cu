@@ -619,6 +619,10 @@ extern "C" int ckpt_create(int device, const ckpt_options *o, ckpt_ctx **out) {
         return rc;
     }
     cudaDeviceGetAttribute(&c->sm_count, cudaDevAttrMultiProcessorCount, device);
+    if (cudaError_t e = preload_kernels(); e != cudaSuccess) {
+        delete c;
+        return fail(CKPT_ECUDA, "create: loading the kernels failed: %s", cudaGetErrorString(e));
+    }
     c->max_ctas = opt.max_ctas ? (int)opt.max_ctas : 2 * c->sm_count;
     int least = 0, greatest = 0;
     cudaDeviceGetStreamPriorityRange(&least, &greatest);
@@ -1910,8 +1914,8 @@ extern "C" int ckpt_load(ckpt_ctx *c, void *stream) {
     if ((rc = prepare_op(c, effective_bucket(c, 0)))) return rc;
     c->seq = saved_seq;  // local op: no group sequence numbers consumed
     CUDA_TRY(cudaEventRecord(c->ev_capture, caller));
-    CUDA_TRY(cudaStreamWaitEvent(c->sC, c->ev_capture, 0));
     const bool from_dev = device_image_valid(c);
+    CUDA_TRY(cudaStreamWaitEvent(from_dev ? c->sP : c->sC, c->ev_capture, 0));
     const uint8_t *img = from_dev ? nullptr : c->hdata[c->completed].p;
     for (uint64_t k = 0; k < c->op_NB; ++k) {
         const uint32_t s = slot_of(c, k);
@@ -1919,12 +1923,13 @@ extern "C" int ckpt_load(ckpt_ctx *c, void *stream) {
         const uint64_t v = valid_in_bucket(c->L, bb, bucket_end(c, k));
         if (!v) continue;
         if (ring_reuse(c, k)) CUDA_TRY(cudaStreamWaitEvent(c->sC, c->ev_kdone[s], 0));
-        if (!from_dev) {
+        if (!from_dev) {  // (from the device copy the unpack needs nothing from the copy stream,
+                          // which may still hold a background host restore)
             CUDA_TRY(cudaMemcpyAsync(slot_ptr(c, c->staging, k), img + bb, v, cudaMemcpyHostToDevice, c->sC));
             c->st.h2d_bytes += v;
+            CUDA_TRY(cudaEventRecord(c->ev_h2d[s], c->sC));
+            CUDA_TRY(cudaStreamWaitEvent(c->sP, c->ev_h2d[s], 0));
         }
-        CUDA_TRY(cudaEventRecord(c->ev_h2d[s], c->sC));
-        CUDA_TRY(cudaStreamWaitEvent(c->sP, c->ev_h2d[s], 0));
         if ((rc = do_pack(c, k, slot_ptr(c, c->staging, k), c->sP, true))) return rc;
         CUDA_TRY(cudaEventRecord(c->ev_kdone[s], c->sP));
     }

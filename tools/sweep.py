@@ -120,12 +120,20 @@ def main():
                 t0 = time.perf_counter()
                 C.ckpt_recover(ctx, mask)
                 t1 = time.perf_counter()
+                h2d0 = C.ckpt_get_stats(ctx)["h2d_bytes"]
                 C.ckpt_load(ctx, st0)
                 st0.synchronize()  # the training stream is ready (a background host restore may continue)
                 t2 = time.perf_counter()
                 C.ckpt_sync(ctx)
                 t3 = time.perf_counter()
                 rb, ld, hs = amax(t1 - t0), amax(t2 - t1), amax(t3 - t0)
+                per = [t2 - t1, float(C.ckpt_get_stats(ctx)["h2d_bytes"] - h2d0)]
+                if world > 1:
+                    g_ = [torch.zeros(2, dtype=torch.float64, device=dev) for _ in range(world)]
+                    dist.all_gather(g_, torch.tensor(per, dtype=torch.float64, device=dev))
+                    per_rank = [(round(x[0].item() * 1e3, 1), int(x[1].item())) for x in g_]
+                else:
+                    per_rank = [(round(per[0] * 1e3, 1), int(per[1]))]
                 srb = C.ckpt_get_stats(ctx)
                 # bit-exact: every tensor of every rank equals the generator (sampled bytes)
                 ok = True
@@ -140,6 +148,7 @@ def main():
                 kgbs = (srb["rebuild_bytes_in"] + srb["rebuild_bytes_out"]) / max(srb["rebuild_ms"], 1e-9) / 1e6
                 rec.setdefault("drill", []).append({"lost": k, "rebuild_ms": round(rb * 1e3, 2), "load_ms": round(ld * 1e3, 2),
                                                     "host_reprotected_ms": round(hs * 1e3, 2),
+                                                    "load_ms_h2d_bytes_per_rank": per_rank,
                                                     "bit_exact_sampled": okall,
                                                     "rank0_rebuild_kernel_gbs": round(kgbs, 1) if rank not in k else None,
                                                     "rank0_rebuild_launches": srb["rebuild_launches"]})
