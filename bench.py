@@ -215,7 +215,9 @@ def main():
     specs, ts = make_rank_state(a.config, rank, dev)
     trace("state ready")
     S = sum(s.nbytes for s in specs)
-    flags = (C.CKPT_OPT_TIMING | (C.CKPT_OPT_TMA_PACK if a.pack == "tma" else 0)
+    # HOST_LOAD: e2e's ckpt_load must restore from the host image (an H2D per step), never
+    # from the still-valid device copy; it does not touch the snapshot path
+    flags = (C.CKPT_OPT_TIMING | C.CKPT_OPT_HOST_LOAD | (C.CKPT_OPT_TMA_PACK if a.pack == "tma" else 0)
              | (C.CKPT_OPT_CE_PACK if a.pack == "ce" else 0) | (C.CKPT_OPT_CE_GATHER if a.gather == "ce" else 0)
              | (C.CKPT_OPT_DEVICE_ONLY if a.device_only else 0))
     if a.device_only:
@@ -255,10 +257,10 @@ def main():
     m = g["m"]
     stream = torch.cuda.current_stream()
 
-    # host-link roofline, measured live: pinned D2H of 4 GiB by every rank at once
-    # (barrier-aligned; the slowest rank's rate is what a synchronous step can get)
+    # host-link roofline, measured live: D2H of 4 GiB by every rank at once (barrier-
+    # aligned) into host memory of the same kind as the arena (THP mmap + cudaHostRegister)
     nprobe = 4 << 30
-    hb = torch.empty(nprobe, dtype=torch.uint8, pin_memory=True)
+    hb = registered_host_buffer(torch, nprobe)
     db = torch.empty(nprobe, dtype=torch.uint8, device=dev)
     best = 0.0
     for _ in range(3):
@@ -271,7 +273,8 @@ def main():
         e1.synchronize()
         best = max(best, nprobe / e0.elapsed_time(e1) / 1e6)
     d2h_peak = best
-    del db, hb
+    del db
+    hb.release()
 
     def step():
         sid = C.ckpt_snapshot(ctx, a.bucket, stream)
@@ -370,7 +373,7 @@ def main():
         # pack (+ copy-engine gather of the peer units when protected)
         o2 = C.ckpt_options_default(n_slots=a.n_slots, bucket_bytes=a.bucket, stripe_unit=a.unit,
                                     host_buffers=host_buffers,
-                                    flags=C.CKPT_OPT_TIMING | C.CKPT_OPT_CE_PACK
+                                    flags=C.CKPT_OPT_TIMING | C.CKPT_OPT_HOST_LOAD | C.CKPT_OPT_CE_PACK
                                     | (C.CKPT_OPT_CE_GATHER if world > 1 else 0))
         ctx2 = C.ckpt_create(local, o2)
         C.ckpt_register(ctx2, descriptors(ts, specs))
@@ -413,6 +416,40 @@ def main():
     if world > 1:
         dist.destroy_process_group()
     return 0
+
+
+class _Registered:
+    """Anonymous THP mmap + cudaHostRegister (the library's arena kind) as a torch tensor."""
+
+    def __init__(self, torch, n):
+        import ctypes
+        import mmap
+        self.m = mmap.mmap(-1, n, flags=mmap.MAP_PRIVATE | mmap.MAP_ANONYMOUS)
+        try:
+            self.m.madvise(mmap.MADV_HUGEPAGE)
+        except Exception:
+            pass
+        self.buf = (ctypes.c_uint8 * n).from_buffer(self.m)
+        ctypes.memset(self.buf, 0, n)
+        self.ptr = ctypes.addressof(self.buf)
+        self.cudart = torch.cuda.cudart()
+        r = self.cudart.cudaHostRegister(self.ptr, n, 1)
+        if int(r) != 0:
+            raise RuntimeError(f"cudaHostRegister failed: {r}")
+        self.t = torch.frombuffer(self.buf, dtype=torch.uint8)
+
+    def copy_(self, src, non_blocking=True):
+        return self.t.copy_(src, non_blocking=non_blocking)
+
+    def release(self):
+        self.cudart.cudaHostUnregister(self.ptr)
+        del self.t
+        del self.buf
+        self.m.close()
+
+
+def registered_host_buffer(torch, n):
+    return _Registered(torch, n)
 
 
 def gemm_corun(torch, C, ctx, stream, bucket, barrier, allmax, dev):
