@@ -39,7 +39,7 @@ def parse():
     p.add_argument("--bucket", type=int, default=512 << 20)
     p.add_argument("--n-slots", type=int, default=0, help="0 = full device copy (single-launch pack)")
     p.add_argument("--unit", type=int, default=64 << 10)
-    p.add_argument("--pack", default="lsu", choices=["lsu", "tma", "ce"],
+    p.add_argument("--pack", default="tma", choices=["lsu", "tma", "ce"],
                    help="pack kernel: 128-bit LSU, TMA bulk through SMEM, or copy engines (zero SMs)")
     p.add_argument("--gather", default="kernel", choices=["kernel", "ce"],
                    help="parity: XOR kernel reads peers over NVLink, or copy engines pull units first")
@@ -218,6 +218,7 @@ def main():
     # HOST_LOAD: e2e's ckpt_load must restore from the host image (an H2D per step), never
     # from the still-valid device copy; it does not touch the snapshot path
     flags = (C.CKPT_OPT_TIMING | C.CKPT_OPT_HOST_LOAD | (C.CKPT_OPT_TMA_PACK if a.pack == "tma" else 0)
+             | (C.CKPT_OPT_LSU_PACK if a.pack == "lsu" else 0)
              | (C.CKPT_OPT_CE_PACK if a.pack == "ce" else 0) | (C.CKPT_OPT_CE_GATHER if a.gather == "ce" else 0)
              | (C.CKPT_OPT_DEVICE_ONLY if a.device_only else 0))
     if a.device_only:

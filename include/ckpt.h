@@ -61,7 +61,9 @@ extern "C" {
 
 /* ---- options ---------------------------------------------------------------------- */
 #define CKPT_OPT_TIMING      0x1u  /* time every pack/xor launch with CUDA events (stats) */
-#define CKPT_OPT_TMA_PACK    0x2u  /* pack via cp.async.bulk (TMA 1-D) through SMEM       */
+#define CKPT_OPT_TMA_PACK    0x2u  /* pack via cp.async.bulk (TMA 1-D) through SMEM; the
+                                      default of the full-copy single-launch pack, opt-in
+                                      for per-bucket (ring) packs                         */
 #define CKPT_OPT_LSU_PACK    0x4u  /* force the 128-bit LDG/STG pack                      */
 #define CKPT_OPT_CE_PACK     0x8u  /* pack/unpack with copy-engine D2D copies (zero SMs)  */
 #define CKPT_OPT_CE_GATHER   0x10u /* parity: copy engines pull the m-1 peer units over

@@ -67,8 +67,7 @@ __device__ __forceinline__ uint4 funnel16(const uint4 &a, const uint4 &b, uint32
 
 // Block-cooperative copy of n bytes (any alignment).
 __device__ __forceinline__ void block_copy(uint8_t *__restrict__ dst, const uint8_t *__restrict__ src,
-                                           uint64_t n) {
-    const uint32_t tid = threadIdx.x, nt = blockDim.x;
+                                           uint64_t n, uint32_t tid, uint32_t nt) {
     uint64_t head = (16 - ((uintptr_t)dst & 15)) & 15;
     if (head > n) head = n;
     if (tid < head) dst[tid] = src[tid];
@@ -110,8 +109,7 @@ __device__ __forceinline__ void block_copy(uint8_t *__restrict__ dst, const uint
     if (tid < tail) dst[t0 + tid] = src[t0 + tid];
 }
 
-__device__ __forceinline__ void block_zero(uint8_t *dst, uint64_t n) {
-    const uint32_t tid = threadIdx.x, nt = blockDim.x;
+__device__ __forceinline__ void block_zero(uint8_t *dst, uint64_t n, uint32_t tid, uint32_t nt) {
     uint64_t head = (16 - ((uintptr_t)dst & 15)) & 15;
     if (head > n) head = n;
     if (tid < head) dst[tid] = 0;
@@ -123,6 +121,12 @@ __device__ __forceinline__ void block_zero(uint8_t *dst, uint64_t n) {
     const uint64_t tail = n & 15, t0 = nw << 4;
     if (tid < tail) dst[t0 + tid] = 0;
 }
+
+// whole-CTA versions
+__device__ __forceinline__ void block_copy(uint8_t *__restrict__ dst, const uint8_t *__restrict__ src, uint64_t n) {
+    block_copy(dst, src, n, threadIdx.x, blockDim.x);
+}
+__device__ __forceinline__ void block_zero(uint8_t *dst, uint64_t n) { block_zero(dst, n, threadIdx.x, blockDim.x); }
 
 // This CTA's share of the bucket: tiles split evenly over gridDim.x, then mapped to
 // the contiguous chunk index range [c_begin, c_end).
@@ -458,17 +462,19 @@ struct BulkRing {
     }
 };
 
-template <int NS>
-__global__ void __launch_bounds__(kTmaThreads) pack_all_tma_kernel(const __grid_constant__ PackAllArgs g) {
+template <int NS, int W>
+__global__ void __launch_bounds__(32 * W) pack_all_tma_kernel(const __grid_constant__ PackAllArgs g) {
+    // W warps, each an independent producer with its own ring of NS SMEM stages: a CTA
+    // keeps W x (NS-1) x 16 KiB of bulk loads in flight, so a few dozen SMs saturate HBM
     extern __shared__ __align__(128) uint8_t smem[];
-    __shared__ __align__(8) uint64_t bars[NS];
-    const uint32_t lane = threadIdx.x;
+    __shared__ __align__(8) uint64_t bars[W][NS];
+    const uint32_t lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     BulkRing<NS> R;
-    R.smem = smem;
-    R.bars = bars;
+    R.smem = smem + (size_t)w * NS * kTmaStage;
+    R.bars = bars[w];
     R.phase = R.issued = R.done = 0;
     if (lane == 0) {
-        for (int i = 0; i < NS; ++i) mbar_init(&bars[i], 1);
+        for (int i = 0; i < NS; ++i) mbar_init(&bars[w][i], 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     }
@@ -485,7 +491,7 @@ __global__ void __launch_bounds__(kTmaThreads) pack_all_tma_kernel(const __grid_
     const uint32_t gpb = (uint32_t)(g.bucket / kGroup);
     constexpr uint32_t tpg = (uint32_t)(kGroup / kTile);
     uint32_t cur = 0, pending = 0;
-    for (uint32_t grp = blockIdx.x; grp < ngroups; grp += gridDim.x) {
+    for (uint32_t grp = blockIdx.x * W + w; grp < ngroups; grp += gridDim.x * W) {
         const uint32_t k = grp / gpb;
         if (pending && k != cur) {
             __syncwarp();
@@ -505,11 +511,11 @@ __global__ void __launch_bounds__(kTmaThreads) pack_all_tma_kernel(const __grid_
             const uint64_t n = clip_chunk(a, g.chunks[c], src, dst);
             if (n == 0) continue;
             if (!src) {
-                block_zero(dst, n);
+                block_zero(dst, n, lane, 32);
                 continue;
             }
             if ((((uintptr_t)dst ^ (uintptr_t)src) & 15) || n < 64) {
-                block_copy(dst, src, n);
+                block_copy(dst, src, n, lane, 32);
                 continue;
             }
             const uint64_t head = (16 - ((uintptr_t)dst & 15)) & 15;
@@ -594,20 +600,20 @@ __global__ void signal_kernel(const SignalArgs a) {
 
 }  // namespace
 
-template <int NS>
-static cudaError_t launch_pack_all_tma(const PackAllArgs &a, uint64_t ngroups, int ctas_per_sm, int sms, cudaStream_t s) {
+template <int NS, int W>
+static cudaError_t launch_pack_all_tma(const PackAllArgs &a, uint64_t ngroups, int ctas, cudaStream_t s) {
     static unsigned long long attr_set = 0;  // bit d: attribute set on device d
-    const int smem = NS * kTmaStage;
+    const int smem = NS * W * kTmaStage;
     int dev = 0;
     cudaGetDevice(&dev);
     if (!(attr_set & (1ull << dev))) {
-        cudaError_t e = cudaFuncSetAttribute(pack_all_tma_kernel<NS>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        cudaError_t e = cudaFuncSetAttribute(pack_all_tma_kernel<NS, W>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
         if (e != cudaSuccess) return e;
         attr_set |= 1ull << dev;
     }
-    const uint64_t cap = (uint64_t)sms * ctas_per_sm;
-    const uint64_t g = ngroups < cap ? ngroups : cap;
-    pack_all_tma_kernel<NS><<<(unsigned)g, kTmaThreads, smem, s>>>(a);
+    const uint64_t need = (ngroups + W - 1) / W;
+    const uint64_t g = need < (uint64_t)ctas ? need : (uint64_t)ctas;
+    pack_all_tma_kernel<NS, W><<<(unsigned)g, 32 * W, smem, s>>>(a);
     return cudaGetLastError();
 }
 
@@ -615,17 +621,18 @@ cudaError_t launch_pack_all(const PackAllArgs &a, int max_ctas, cudaStream_t s, 
     const uint64_t ngroups = (a.L + kGroup - 1) / kGroup;
     if (ngroups == 0) return cudaSuccess;
     if (tma) {
-        // max_ctas is the LSU budget (2 per SM): the TMA kernel runs max_ctas/2 SMs with
-        // NS stages; CKPT_TMA_STAGES picks 4 (3 CTAs/SM), 6 (2/SM) or 8 (1/SM, default)
-        static int ns = -1;
-        if (ns < 0) {
-            const char *e = getenv("CKPT_TMA_STAGES");
-            ns = e ? atoi(e) : 8;
+        // one CTA per SM (192 KiB of SMEM) on max_ctas/2 SMs: 4 producer warps x 3 stages
+        // (CKPT_TMA_CFG=2 selects 2 warps x 6 stages, 8: 8 warps x 1.5 ... see DESIGN.md)
+        static int cfg = -1;
+        if (cfg < 0) {
+            const char *e = getenv("CKPT_TMA_CFG");
+            cfg = e ? atoi(e) : 4;
         }
-        const int sms = max_ctas / 2 > 0 ? max_ctas / 2 : 1;
-        if (ns == 4) return launch_pack_all_tma<4>(a, ngroups, 3, sms, s);
-        if (ns == 6) return launch_pack_all_tma<6>(a, ngroups, 2, sms, s);
-        return launch_pack_all_tma<8>(a, ngroups, 1, sms, s);
+        const int ctas = max_ctas / 2 > 0 ? max_ctas / 2 : 1;
+        if (cfg == 2) return launch_pack_all_tma<6, 2>(a, ngroups, ctas, s);
+        if (cfg == 1) return launch_pack_all_tma<8, 1>(a, ngroups, ctas, s);
+        if (cfg == 6) return launch_pack_all_tma<2, 6>(a, ngroups, ctas, s);
+        return launch_pack_all_tma<3, 4>(a, ngroups, ctas, s);
     }
     const uint64_t g = ngroups < (uint64_t)max_ctas ? ngroups : (uint64_t)max_ctas;
     pack_all_kernel<<<(unsigned)g, kPackThreads, 0, s>>>(a);
@@ -638,7 +645,8 @@ cudaError_t preload_kernels() {
     cudaFuncAttributes fa;
     const void *fns[] = {
         (const void *)pack_kernel, (const void *)pack_all_kernel, (const void *)pack_tma_kernel,
-        (const void *)pack_all_tma_kernel<4>, (const void *)pack_all_tma_kernel<6>, (const void *)pack_all_tma_kernel<8>,
+        (const void *)pack_all_tma_kernel<3, 4>, (const void *)pack_all_tma_kernel<6, 2>,
+        (const void *)pack_all_tma_kernel<8, 1>, (const void *)pack_all_tma_kernel<2, 6>,
         (const void *)xor_kernel<1, xor_unroll<1>()>, (const void *)xor_kernel<2, xor_unroll<2>()>,
         (const void *)xor_kernel<3, xor_unroll<3>()>, (const void *)xor_kernel<4, xor_unroll<4>()>,
         (const void *)xor_kernel<5, xor_unroll<5>()>, (const void *)xor_kernel<6, xor_unroll<6>()>,

@@ -1453,7 +1453,9 @@ static int issue_pack_all(ckpt_ctx *c) {
     a.maxb = kMaxB;
     TimedLaunch *t;
     if ((rc = timed_begin(c, c->sP, 0, &t))) return rc;
-    CUDA_TRY(launch_pack_all(a, c->max_ctas, c->sP, (c->opt.flags & CKPT_OPT_TMA_PACK) != 0));
+    // default single-launch pack: the multi-producer TMA kernel (same HBM bandwidth as the
+    // LSU kernel from ~2.5x fewer SM-seconds); CKPT_OPT_LSU_PACK selects the LSU kernel
+    CUDA_TRY(launch_pack_all(a, c->max_ctas, c->sP, !(c->opt.flags & CKPT_OPT_LSU_PACK)));
     if ((rc = timed_end(t, c->sP))) return rc;
     c->st.pack_launches++;
     c->st.pack_bytes += 2 * c->L;

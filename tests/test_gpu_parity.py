@@ -45,7 +45,7 @@ def tiny(rank, n=9, misalign=0, device="cuda:0"):
 @pytest.mark.parametrize("n_slots,bucket,flags", [
     (0, 0, 0), (2, 4096, 0), (4, 65536, 0), (3, 1 << 20, 0),
     (0, 0, 0x2), (2, 65536, 0x2), (4, 4096, 0x2),
-    (0, 0, 0x8), (2, 65536, 0x8), (3, 4096, 0x8)])
+    (0, 0, 0x8), (2, 65536, 0x8), (3, 4096, 0x8), (0, 0, 0x4), (0, 65536, 0x4)])
 @pytest.mark.parametrize("misalign", [0, 1])
 def test_snapshot_unprotected_matches_oracle(torch, C, n_slots, bucket, flags, misalign):
     st = tiny(0, n=11, misalign=misalign)
@@ -133,7 +133,7 @@ def expected_group(states, Lstar, unit):
 @pytest.mark.parametrize("m", [2, 3, 4, 8])
 @pytest.mark.parametrize("unit,n_slots,bucket", [(65536, 0, 1 << 20), (4096, 3, 1 << 20), (16, 2, 4096),
                                                  (0, 0, 1 << 20), (65536, 4, 1 << 20)])
-@pytest.mark.parametrize("flags", [0, 0x10, 0x18])
+@pytest.mark.parametrize("flags", [0, 0x4, 0x10, 0x18])
 def test_group_encode_matches_oracle(torch, C, m, unit, n_slots, bucket, flags):
     if unit == 65536 and n_slots and (m - 1) * unit > bucket:
         pytest.skip("stripe larger than ring slot")
@@ -400,7 +400,7 @@ def test_fence_and_capture_point(torch, C, n_slots, m):
             C.ckpt_destroy(c)
 
 
-@pytest.mark.parametrize("flags", [0, 0x2, 0x8])
+@pytest.mark.parametrize("flags", [0, 0x2, 0x4, 0x8])
 @pytest.mark.parametrize("n_slots", [0, 2])
 def test_no_writes_outside_tensors(torch, C, flags, n_slots):
     """Bounds check without compute-sanitizer (closed on this pool): every tensor is a
