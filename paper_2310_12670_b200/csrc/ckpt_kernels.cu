@@ -690,12 +690,12 @@ cudaError_t launch_pack(const PackArgs &a, int max_ctas, cudaStream_t s, bool tm
 
 cudaError_t launch_xor(const XorArgs &a, int max_ctas, cudaStream_t s) {
     if (a.nstripes == 0 || a.nin < 1 || a.nin > kMaxTerms || (a.unit & 15)) return cudaErrorInvalidValue;
-    static int mult = -1;  // CTAs per (pack) CTA budget: more warps hide NVLink latency
-    if (mult < 0) {
-        const char *e = getenv("CKPT_XOR_GRID_MULT");
-        mult = e ? std::max(1, atoi(e)) : 1;
+    static int cap = -1;  // CKPT_XOR_CTAS: CTA budget of the XOR kernel (0 = the pack's)
+    if (cap < 0) {
+        const char *e = getenv("CKPT_XOR_CTAS");
+        cap = e ? std::max(0, atoi(e)) : 0;
     }
-    max_ctas *= mult;
+    if (cap > 0) max_ctas = cap;
     switch (a.nin) {
         case 1: return launch_xor_n<1>(a, max_ctas, s);
         case 2: return launch_xor_n<2>(a, max_ctas, s);
