@@ -46,6 +46,8 @@ def parse():
     p.add_argument("--device-only", action="store_true",
                    help="CKPT_OPT_DEVICE_ONLY: device-side protect only (pack + parity into HBM, no D2H)")
     p.add_argument("--max-ctas", type=int, default=0, help="CTA budget of a pack/XOR launch (0 = 2 x SMs)")
+    p.add_argument("--group-size", type=int, default=0,
+                   help="protection group size m (0 = all N ranks); N/m disjoint node subgroups")
     p.add_argument("--scheme", default="aec", choices=["aec", "arc", "arc_aec"],
                    help="protection: AEC parity (default), ARC ring copies, or both (collaborative)")
     p.add_argument("--no-corun", action="store_true", help="skip the co-running GEMM measurement")
@@ -227,15 +229,16 @@ def main():
     # neighbour: L (+ L/(m-1))]; fall back to one buffer if the node's available memory
     # (and /dev/shm for the ARC schemes), all ranks together +25%, would not hold two
     scheme = {"aec": C.CKPT_SCHEME_AEC, "arc": C.CKPT_SCHEME_ARC, "arc_aec": C.CKPT_SCHEME_ARC_AEC}[a.scheme]
-    P = S // (world - 1) if world > 1 and a.scheme != "arc" else 0
-    per_buf = S + P + ((S + P) if a.scheme != "aec" and world > 1 else 0)
+    Gm = a.group_size or world
+    P = S // (Gm - 1) if Gm > 1 and a.scheme != "arc" else 0
+    per_buf = S + P + ((S + P) if a.scheme != "aec" and Gm > 1 else 0)
     host_buffers = 2
     try:
         avail = int([l for l in open("/proc/meminfo") if l.startswith("MemAvailable")][0].split()[1]) * 1024
         if a.scheme != "aec":
             st_shm = os.statvfs("/dev/shm")
             avail = min(avail, st_shm.f_bavail * st_shm.f_frsize)
-        if world * 2 * per_buf * 1.25 + world * (4 << 30) > avail:
+        if world * 2 * per_buf * 1.25 + world * (4 << 30) > avail:  # all ranks of the node
             host_buffers = 1
     except Exception:
         pass
@@ -248,8 +251,17 @@ def main():
     C.ckpt_register(ctx, descriptors(ts, specs), {"rank": rank, "world": world, "local_rank": local,
                                                   "local_world": world, "tp_rank": rank, "tp_size": 8,
                                                   "pp_rank": 0, "pp_size": 1, "dp_rank": 0, "dp_size": 1})
-    if world > 1:
-        C.protect_ipc(ctx, scheme=scheme)
+    G = a.group_size or world
+    if world % G:
+        raise SystemExit(f"--group-size {G} must divide N = {world}")
+    sub = None
+    if world > 1 and G < world:  # disjoint subgroups of G consecutive ranks
+        for s0 in range(0, world, G):
+            grp = dist.new_group(list(range(s0, s0 + G)))
+            if s0 <= rank < s0 + G:
+                sub = grp
+    if world > 1 and G > 1:
+        C.protect_ipc(ctx, group=sub, scheme=scheme)
     else:
         C.ckpt_protect(ctx, 1, 0)  # EUNAVAIL: snapshot only, allocates the host arena
     t_setup = time.perf_counter() - t_setup
@@ -375,11 +387,11 @@ def main():
         o2 = C.ckpt_options_default(n_slots=a.n_slots, bucket_bytes=a.bucket, stripe_unit=a.unit,
                                     host_buffers=host_buffers,
                                     flags=C.CKPT_OPT_TIMING | C.CKPT_OPT_HOST_LOAD | C.CKPT_OPT_CE_PACK
-                                    | (C.CKPT_OPT_CE_GATHER if world > 1 else 0))
+                                    | (C.CKPT_OPT_CE_GATHER if world > 1 and G > 1 else 0))
         ctx2 = C.ckpt_create(local, o2)
         C.ckpt_register(ctx2, descriptors(ts, specs))
-        if world > 1:
-            C.protect_ipc(ctx2)
+        if world > 1 and G > 1:
+            C.protect_ipc(ctx2, group=sub)
         else:
             C.ckpt_protect(ctx2, 1, 0)
         corun["ce_pack"] = gemm_corun(torch, C, ctx2, stream, a.bucket, barrier, allmax, dev)
@@ -401,7 +413,7 @@ def main():
                        "m": m, "L_star": g["L_star"], "stripe_unit": g["unit"], "bucket_bytes": a.bucket,
                        "n_slots": a.n_slots, "pack": a.pack, "gather": a.gather, "device_only": a.device_only,
                        "max_ctas": a.max_ctas or "2 x SMs", "host_buffers": host_buffers,
-                       "scheme": a.scheme,
+                       "scheme": a.scheme, "groups": f"{world // (a.group_size or world)} x m={a.group_size or world}",
                        "l2": f"inputs {S / 1e9:.2f} GB/GPU >> 126 MB L2; no flush needed"},
             "per_gpu_gbs": round(value / N, 3),
             "host_link": None if a.device_only else {

@@ -337,3 +337,99 @@ def test_ipc_arc_schemes(scheme):
                 p.kill()
     for rank, ok, _ in res:
         assert all(ok), (rank, "failed checks (case index)", [i for i, x in enumerate(ok) if not x])
+
+
+def _worker_sub(rank, world, port, q, G):
+    try:
+        os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank), WORLD_SIZE=str(world))
+        import torch
+        import torch.distributed as dist
+
+        import oracle
+        import synth
+        from paper_2310_12670_b200 import ckpt as C
+        from synth.gpu import descriptors, fill_state, make_rank_state
+
+        torch.cuda.set_device(rank)
+        dev = torch.device("cuda", rank)
+        dist.init_process_group("nccl", device_id=dev)
+        sub = None
+        for s0 in range(0, world, G):
+            grp = dist.new_group(list(range(s0, s0 + G)))
+            if s0 <= rank < s0 + G:
+                sub, base = grp, s0
+        specs, ts = make_rank_state("tiny_7", rank, dev, misalign=1)
+        ctx = C.ckpt_create(rank, C.ckpt_options_default(stripe_unit=4096, n_slots=0, bucket_bytes=1 << 16))
+        C.ckpt_register(ctx, descriptors(ts, specs))
+        C.protect_ipc(ctx, group=sub)
+        g = C.ckpt_geometry(ctx)
+        sid = C.ckpt_snapshot(ctx)
+        C.ckpt_wait(ctx, sid)
+        imgs = []
+        for j in range(base, base + G):
+            sp = synth.config_tensors("tiny_7", j)
+            tb = [synth.fill(synth.SEED, j, t, s.nbytes) for t, s in enumerate(sp)]
+            off, _ = oracle.layout([s.nbytes for s in sp])
+            imgs.append(oracle.pack(tb, off, g["L_star"]))
+        me = rank - base
+        d, p = C.ckpt_host_view(ctx, 0, copy=True)
+        ok = [g["m"] == G, bool(np.array_equal(d, imgs[me])), bool(np.array_equal(p, oracle.encode(imgs, g["unit"], me)))]
+        # one loss in EVERY subgroup at once (member 0 of each), recovered independently
+        fill_state(ts, rank, seed=9, xor_mode=1)
+        if me == 0:
+            C.ckpt_forget(ctx, 0xA5)
+            for t in ts:
+                t.view(torch.uint8).fill_(0xA5)
+        dist.barrier()
+        C.ckpt_rebuild(ctx, 0)
+        C.ckpt_load(ctx)
+        torch.cuda.synchronize()
+        good = True
+        for t, x in enumerate(ts):
+            got = x.contiguous().view(torch.uint8).cpu().numpy()
+            good = good and np.array_equal(got, synth.fill(synth.SEED, rank, t, specs[t].nbytes))
+        ok.append(bool(good))
+        dist.barrier()
+        C.ckpt_destroy(ctx)
+        dist.barrier()
+        dist.destroy_process_group()
+        q.put((rank, ok, None))
+    except Exception:
+        q.put((rank, None, traceback.format_exc()))
+
+
+def test_ipc_disjoint_subgroups():
+    """SURVEY 8(e): the node's ranks split into disjoint protection groups (here pairs);
+    each group encodes its own parity, and one loss per group is recovered concurrently."""
+    world = min(_world(), 8)
+    if world < 4:
+        pytest.skip("needs >= 4 GPUs for two groups of two")
+    world -= world % 2
+    import queue
+    import time
+
+    import torch.multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    ps = [ctx.Process(target=_worker_sub, args=(r, world, port, q, 2)) for r in range(world)]
+    for p in ps:
+        p.start()
+    res, t0 = [], time.time()
+    try:
+        while len(res) < world:
+            try:
+                r = q.get(timeout=5)
+            except queue.Empty:
+                assert all(p.exitcode in (None, 0) for p in ps), "worker died"
+                assert time.time() - t0 < 300, "timed out"
+                continue
+            assert r[2] is None, r[2]
+            res.append(r)
+    finally:
+        for p in ps:
+            p.join(30)
+            if p.is_alive():
+                p.kill()
+    for rank, ok, _ in res:
+        assert all(ok), (rank, ok)
