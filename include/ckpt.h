@@ -77,6 +77,9 @@ extern "C" {
 #define CKPT_OPT_HOST_LOAD   0x80u /* always restore (load / rebuild sources) from the host
                                       image, never from a still-valid device copy (the
                                       paper's REFT-load after a full restart, P.545)       */
+#define CKPT_OPT_WINDOWED    0x100u /* HAS placement (Alg 1, P.377-429): each bucket's D2H
+                                      waits until the caller's training stream has opened
+                                      the snapshot window (ckpt_window)                   */
 #define CKPT_OPT_SHM_ARENA   0x40u /* host arena in POSIX shared memory (/dev/shm), one file
                                       per member and host buffer: peers (ARC) and a restarted
                                       process can reach it; required by the ARC schemes     */
@@ -324,6 +327,30 @@ int ckpt_plan_common(const uint64_t *Lj, uint32_t m, uint64_t unit, uint64_t *L_
 /* Remove the persistent arena of `key` (members [0, m), host buffers [0, nbuf)) from
  * /dev/shm.  Host-only; missing objects are ignored. */
 int ckpt_arena_unlink(uint64_t key, uint32_t m, uint32_t nbuf);
+
+/* ---- Hierarchical Asynchronous Snapshotting (Alg 1, P.377-429) ------------------------
+ * Placement of the snapshot's host traffic relative to training.  With copy engines the
+ * D2H can overlap anything; what it still disturbs is HBM-bound training work (measured:
+ * a concurrent 57 GB/s D2H slows an HBM-bound kernel by 10-35%, tools/ce_interference.py).
+ * ckpt_window(ctx, open, stream) enqueues on the TRAINING stream a write of the
+ * context's window flag (1 = open, 0 = closed; open at creation).  With CKPT_OPT_WINDOWED
+ * every bucket's D2H first waits (on the copy engine's stream, zero SMs) for an open
+ * window, so the caller opens it around bubbles and compute-bound phases (layers 1 and 2)
+ * and closes it around HBM-bound phases.  A snapshot whose window is never reopened does
+ * not complete (ckpt_wait times out). */
+int ckpt_window(ckpt_ctx *ctx, int open, void *stream);
+
+/* Alg 1's estimators, host-only.  EstimateSnapshotTime = bytes / B_io; EstimateBubbleTime
+ * = (0.8 p + 2|P| - p - 2) * C_FB,BP (1F1B, stage p of |P|, clamped at 0); SplitParameter:
+ * if t_ss >= t_bubble the first floor(n * t_bubble / t_ss) of n bytes go into bubbles and
+ * the rest alongside computation, else all n bytes go into bubbles. */
+typedef struct ckpt_has_plan_t {
+    double t_ss, t_bubble;        /* seconds                                             */
+    uint64_t bubble_bytes;        /* W_bubble (Alg 1 line 10/12)                          */
+    uint64_t compute_bytes;       /* W_* (snapshotted during computation)                 */
+} ckpt_has_plan_t;
+int ckpt_has_plan(uint32_t stage, uint32_t num_stages, double c_fb_bp_s, uint64_t snapshot_bytes,
+                  double b_io_bytes_per_s, ckpt_has_plan_t *out);
 
 /* Library version string, e.g. "reft-ckpt 0.1 sm_100a". */
 const char *ckpt_version(void);

@@ -37,6 +37,7 @@ CKPT_OPT_CE_GATHER = 0x10
 CKPT_OPT_DEVICE_ONLY = 0x20
 CKPT_OPT_SHM_ARENA = 0x40
 CKPT_OPT_HOST_LOAD = 0x80
+CKPT_OPT_WINDOWED = 0x100
 CKPT_SCHEME_DEFAULT, CKPT_SCHEME_AEC, CKPT_SCHEME_ARC, CKPT_SCHEME_ARC_AEC = 0, 1, 2, 3
 
 CKPT_DTYPE_BYTES, CKPT_DTYPE_BF16, CKPT_DTYPE_FP16, CKPT_DTYPE_FP32 = 0, 1, 2, 3
@@ -84,6 +85,11 @@ class ckpt_stats(ctypes.Structure):
         return {n: getattr(self, n) for n, _ in self._fields_}
 
 
+class ckpt_has_plan_t(ctypes.Structure):
+    _fields_ = [("t_ss", ctypes.c_double), ("t_bubble", ctypes.c_double), ("bubble_bytes", _u64),
+                ("compute_bytes", _u64)]
+
+
 class CkptError(RuntimeError):
     def __init__(self, code: int, where: str, msg: str):
         self.code = code
@@ -118,6 +124,9 @@ def lib():
             "ckpt_rebuild": (ctypes.c_int, [_vp, _i32, _vp]),
             "ckpt_recover": (ctypes.c_int, [_vp, _u32, _vp]),
             "ckpt_sync": (ctypes.c_int, [_vp]),
+            "ckpt_window": (ctypes.c_int, [_vp, ctypes.c_int, _vp]),
+            "ckpt_has_plan": (ctypes.c_int, [_u32, _u32, ctypes.c_double, _u64, ctypes.c_double,
+                                             ctypes.POINTER(ckpt_has_plan_t)]),
             "ckpt_forget": (ctypes.c_int, [_vp, ctypes.c_uint8]),
             "ckpt_host_view": (ctypes.c_int, [_vp, ctypes.c_int, ctypes.POINTER(_vp), ctypes.POINTER(_u64),
                                               ctypes.POINTER(_vp), ctypes.POINTER(_u64)]),
@@ -271,6 +280,20 @@ def ckpt_rebuild(ctx: int, lost_rank: int, stream=None) -> None:
 
 def ckpt_recover(ctx: int, lost_mask: int, stream=None) -> None:
     _check(lib().ckpt_recover(ctx, lost_mask, _stream_handle(stream)), "ckpt_recover")
+
+
+def ckpt_window(ctx: int, open_: bool, stream=None) -> None:
+    """HAS: open/close the snapshot window at the current position of the training stream."""
+    _check(lib().ckpt_window(ctx, 1 if open_ else 0, _stream_handle(stream)), "ckpt_window")
+
+
+def ckpt_has_plan(stage: int, num_stages: int, c_fb_bp_s: float, snapshot_bytes: int, b_io: float) -> dict:
+    """Alg 1's EstimateSnapshotTime / EstimateBubbleTime / SplitParameter (host-only)."""
+    o = ckpt_has_plan_t()
+    _check(lib().ckpt_has_plan(stage, num_stages, c_fb_bp_s, snapshot_bytes, b_io, ctypes.byref(o)),
+           "ckpt_has_plan")
+    return {"t_ss": o.t_ss, "t_bubble": o.t_bubble, "bubble_bytes": o.bubble_bytes,
+            "compute_bytes": o.compute_bytes}
 
 
 def ckpt_sync(ctx: int) -> None:

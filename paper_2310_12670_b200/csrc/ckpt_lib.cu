@@ -17,6 +17,7 @@
 #include <cudaTypedefs.h>
 
 #include <algorithm>
+#include <cmath>
 #include <atomic>
 #include <cstdarg>
 #include <chrono>
@@ -185,6 +186,7 @@ struct ckpt_ctx {
     uint64_t staging_bytes = 0;
     uint32_t *flags = nullptr;  // local flag page (device), written by peers
     uint32_t *counters = nullptr;  // per-bucket CTA completion counters (single-launch pack)
+    uint32_t *window = nullptr;    // HAS window flag (device, bit 0 = open), written by memops
 
     // group
     bool grouped = false;  // ckpt_protect succeeded (m >= 2) or m == 1 arena set up
@@ -641,6 +643,11 @@ extern "C" int ckpt_create(int device, const ckpt_options *o, ckpt_ctx **out) {
         if (e == cudaSuccess) e = cudaEventCreateWithFlags(ev, cudaEventDisableTiming);
     if (e == cudaSuccess) e = cudaEventCreate(&c->ev_t0);
     if (e == cudaSuccess) e = cudaEventCreate(&c->ev_t1);
+    if (e == cudaSuccess) e = cudaMalloc(&c->window, 256);
+    if (e == cudaSuccess) {
+        const uint32_t one = 1;  // windows start open
+        e = cudaMemcpy(c->window, &one, sizeof one, cudaMemcpyHostToDevice);
+    }
     if (e != cudaSuccess) {
         ckpt_destroy(c);
         return fail(CKPT_ECUDA, "create: %s", cudaGetErrorString(e));
@@ -682,6 +689,7 @@ extern "C" int ckpt_destroy(ckpt_ctx *c) {
     if (c->staging) cudaFree(c->staging);
     if (c->flags) cudaFree(c->flags);
     if (c->counters) cudaFree(c->counters);
+    if (c->window) cudaFree(c->window);
     if (c->parity) cudaFree(c->parity);
     if (c->gather) cudaFree(c->gather);
     for (int i = 0; i < 2; ++i) {
@@ -1647,6 +1655,10 @@ static int stage_copy(ckpt_ctx *c, uint64_t k, bool with_parity = true) {
         CUDA_TRY(cudaEventRecord(c->ev_d2h_data[s], c->sC));
         return with_parity ? stage_copy_parity(c, k) : CKPT_OK;
     }
+    if (v && (c->opt.flags & CKPT_OPT_WINDOWED)) {  // HAS: only while the window is open
+        CUresult r = p_wait32((CUstream)c->sC, (CUdeviceptr)(uintptr_t)c->window, 1u, CU_STREAM_WAIT_VALUE_AND);
+        if (r != CUDA_SUCCESS) return fail(CKPT_ECUDA, "cuStreamWaitValue32(window) failed (%d)", (int)r);
+    }
     if (v) {
         CUDA_TRY(cudaMemcpyAsync(c->hdata[c->ongoing].p + bb, slot_ptr(c, c->staging, k), v, cudaMemcpyDeviceToHost, c->sC));
         c->st.d2h_bytes += v;
@@ -1667,6 +1679,10 @@ static int stage_copy_parity(ckpt_ctx *c, uint64_t k) {
     const uint64_t bb = bucket_begin(c, k), be = bucket_end(c, k);
     const uint64_t pb = (be - bb) / (c->m - 1);
     CUDA_TRY(cudaStreamWaitEvent(c->sC, c->ev_xored[s], 0));
+    if (!device_only(c) && (c->opt.flags & CKPT_OPT_WINDOWED)) {
+        CUresult r = p_wait32((CUstream)c->sC, (CUdeviceptr)(uintptr_t)c->window, 1u, CU_STREAM_WAIT_VALUE_AND);
+        if (r != CUDA_SUCCESS) return fail(CKPT_ECUDA, "cuStreamWaitValue32(window) failed (%d)", (int)r);
+    }
     if (!device_only(c)) {
         CUDA_TRY(cudaMemcpyAsync(c->hpar[c->ongoing].p + bb / (c->m - 1), parity_slot_ptr(c, k), pb,
                                  cudaMemcpyDeviceToHost, c->sC));
@@ -2279,6 +2295,31 @@ extern "C" int ckpt_recover(ckpt_ctx *c, uint32_t mask, void *stream) {
     if ((rc = recover_step1(c, mask, c->next_id - 1))) return rc;
     if (rem >= 0 && (rc = rebuild_aec(c, rem, stream))) return rc;
     return recover_step3(c, mask);
+}
+
+// ------------------------------------------------------------------ HAS -------------
+extern "C" int ckpt_window(ckpt_ctx *c, int open, void *stream) {
+    if (!c) return fail(CKPT_EINVAL, "window: null");
+    if (load_memops()) return fail(CKPT_ECUDA, "window: stream memory operations unavailable");
+    int rc = set_dev(c);
+    if (rc) return rc;
+    CUresult r = p_write32((CUstream)stream, (CUdeviceptr)(uintptr_t)c->window, open ? 1u : 0u,
+                           CU_STREAM_WRITE_VALUE_DEFAULT);
+    if (r != CUDA_SUCCESS) return fail(CKPT_ECUDA, "cuStreamWriteValue32(window) failed (%d)", (int)r);
+    return CKPT_OK;
+}
+
+extern "C" int ckpt_has_plan(uint32_t p, uint32_t P, double c, uint64_t bytes, double bio, ckpt_has_plan_t *out) {
+    if (!out || P == 0 || p >= P || c < 0 || bio <= 0) return fail(CKPT_EINVAL, "has_plan: bad args");
+    out->t_ss = (double)bytes / bio;                                          // EstimateSnapshotTime
+    out->t_bubble = std::max(0.0, (0.8 * p + 2.0 * P - p - 2.0) * c);         // EstimateBubbleTime
+    if (out->t_ss >= out->t_bubble && out->t_ss > 0) {                        // SplitParameter
+        out->bubble_bytes = (uint64_t)std::floor((double)bytes * out->t_bubble / out->t_ss);
+    } else {
+        out->bubble_bytes = bytes;
+    }
+    out->compute_bytes = bytes - out->bubble_bytes;
+    return CKPT_OK;
 }
 
 // ------------------------------------------------------------------ misc ------------

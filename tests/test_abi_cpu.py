@@ -89,3 +89,22 @@ def test_strerror_and_version(C):
 def test_options_defaults(C):
     o = C.ckpt_options_default()
     assert (o.align, o.stripe_unit, o.bucket_bytes, o.n_slots, o.host_buffers) == (256, 65536, 64 << 20, 4, 2)
+
+
+def test_has_plan_spec_vectors(C):
+    """Alg 1 (P.377-413) estimators against SPEC's worked examples (S.185-187, S.242-248,
+    S.236): EstimateBubbleTime(p=0,|P|=4,C=1) = 6.0; (p=3,|P|=4,C=2) = 10.8; |P|=1 -> 0;
+    EstimateSnapshotTime(16 GiB at 16 GiB/s) = 1.0 s; SplitParameter(100, t_ss=10,
+    t_bubble=4) = (40, 60); t_ss < t_bubble -> (100, 0); t_bubble = 0 -> (0, 100)."""
+    assert C.ckpt_has_plan(0, 4, 1.0, 1, 1.0)["t_bubble"] == pytest.approx(6.0)
+    assert C.ckpt_has_plan(3, 4, 2.0, 1, 1.0)["t_bubble"] == pytest.approx(10.8)
+    assert C.ckpt_has_plan(0, 1, 5.0, 1, 1.0)["t_bubble"] == 0.0
+    assert C.ckpt_has_plan(0, 1, 1.0, 16 << 30, float(16 << 30))["t_ss"] == pytest.approx(1.0)
+    p = C.ckpt_has_plan(0, 3, 1.0, 100, 10.0)  # t_bubble = (2*3-2)*1 = 4, t_ss = 100/10 = 10
+    assert (p["t_ss"], p["t_bubble"], p["bubble_bytes"], p["compute_bytes"]) == (10.0, 4.0, 40, 60)
+    p = C.ckpt_has_plan(0, 6, 1.0, 100, 20.0)  # t_bubble 10 > t_ss 5
+    assert (p["bubble_bytes"], p["compute_bytes"]) == (100, 0)
+    p = C.ckpt_has_plan(0, 1, 1.0, 100, 10.0)  # no pipeline, no bubble
+    assert (p["bubble_bytes"], p["compute_bytes"]) == (0, 100)
+    with pytest.raises(C.CkptError):
+        C.ckpt_has_plan(4, 4, 1.0, 1, 1.0)

@@ -566,3 +566,28 @@ def test_load_from_device_copy_and_host_path_agree(torch, C):
             C.ckpt_wait(ctx, sid)
         finally:
             C.ckpt_destroy(ctx)
+
+
+def test_has_window_gates_the_d2h(torch, C):
+    """HAS placement (Alg 1 layers): with CKPT_OPT_WINDOWED no bucket reaches host memory
+    while the training stream holds the window closed; once reopened the snapshot
+    completes and matches the oracle."""
+    import time
+    st = tiny(0, n=9)
+    specs, ts = st
+    ctx = make_ctx(C, st, n_slots=0, bucket_bytes=1 << 16, flags=C.CKPT_OPT_WINDOWED)
+    s = torch.cuda.Stream()
+    try:
+        C.ckpt_protect(ctx, 1, 0)
+        C.ckpt_window(ctx, False, s)
+        sid = C.ckpt_snapshot(ctx, 0, s)
+        time.sleep(0.3)
+        d_ongoing, _ = C.ckpt_host_view(ctx, 1, copy=True)
+        assert not d_ongoing.any(), "D2H ran while the window was closed"
+        C.ckpt_window(ctx, True, s)
+        C.ckpt_wait(ctx, sid)
+        g = C.ckpt_geometry(ctx)
+        want, _, _ = oracle_image(specs, 0, g["L_star"])
+        assert_bytes_equal(C.ckpt_host_view(ctx, 0, copy=True)[0], want, "image after the window opened")
+    finally:
+        C.ckpt_destroy(ctx)
