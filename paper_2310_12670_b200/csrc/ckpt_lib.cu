@@ -164,7 +164,7 @@ struct ckpt_ctx {
     ckpt_options opt{};
     int sm_count = 148;
     int max_ctas = 296;
-    int xor_ctas = 74;  // XOR kernels: NVLink-bound, half the SMs reach the same rate
+    int xor_ctas = 296;  // CTA budget of the XOR kernels (CKPT_XOR_CTAS overrides)
     int sticky = CKPT_OK;
     std::string sticky_msg;
 
@@ -627,9 +627,9 @@ extern "C" int ckpt_create(int device, const ckpt_options *o, ckpt_ctx **out) {
         return fail(CKPT_ECUDA, "create: loading the kernels failed: %s", cudaGetErrorString(e));
     }
     c->max_ctas = opt.max_ctas ? (int)opt.max_ctas : 2 * c->sm_count;
-    // measured (N=2, 11.8 GB): 74 CTAs move 660 GB/s of peer reads vs 671 with 296, and
-    // the co-running GEMM loses less; the pack keeps its own budget
-    c->xor_ctas = opt.max_ctas ? (int)opt.max_ctas : std::max(1, c->sm_count / 2);
+    // measured: at m = 2 half the SMs read peers as fast as 2 x SMs (660 vs 671 GB/s), at
+    // m = 4 they do not (497 vs 590 GB/s) -- the XOR keeps the full budget
+    c->xor_ctas = c->max_ctas;
     int least = 0, greatest = 0;
     cudaDeviceGetStreamPriorityRange(&least, &greatest);
     int prio = opt.priority == INT32_MAX ? least : std::min(least, std::max(greatest, (int)opt.priority));
