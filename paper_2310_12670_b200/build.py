@@ -17,11 +17,11 @@ ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
-FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O2,-Wall", "-shared",
+FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O2,-Wall,-fvisibility=hidden", "-shared",
          "-Xptxas", "-v", "-I" + os.path.join(ROOT, "include")]
 
 LIBS = {
-    "libreft_ckpt.so": ["ckpt_lib.cu", "ckpt_kernels.cu"],
+    "libreft_ckpt.so": ["ckpt_api.cu", "ckpt_hostmem.cu", "ckpt_pipeline.cu", "ckpt_recovery.cu", "ckpt_kernels.cu"],
     "libreft_synth.so": ["synth_fill.cu"],
 }
 
@@ -30,7 +30,8 @@ def _stale(out, srcs):
     if not os.path.exists(out):
         return True
     t = os.path.getmtime(out)
-    deps = srcs + [os.path.join(CSRC, "ckpt_kernels.cuh"), os.path.join(ROOT, "include", "ckpt.h"),
+    deps = srcs + [os.path.join(CSRC, "ckpt_kernels.cuh"), os.path.join(CSRC, "ckpt_internal.cuh"),
+                   os.path.join(ROOT, "include", "ckpt.h"),
                    os.path.join(ROOT, "include", "reft_synth.h")]
     return any(os.path.getmtime(d) > t for d in deps)
 

@@ -3,7 +3,9 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#pragma GCC visibility push(default)  // the C ABI is the only exported surface
 #include "../../include/reft_synth.h"
+#pragma GCC visibility pop
 
 namespace {
 __device__ __forceinline__ uint64_t sm64(uint64_t x) {
