@@ -57,10 +57,13 @@ def lib():
         L.oracle_arc_holder.restype = _u64
         L.oracle_arc_copy.argtypes = [_u64, _p, _u64, _u64, _p]
         L.oracle_recover.argtypes = [_u64, _u64, _p, _p, _p, _p, _p, _u64, _u64, _p, _p]
+        L.oracle_aor_update.argtypes = [_u64, _p, _p, _u64, ctypes.c_float]
+        L.oracle_aor_recover.argtypes = [_u64, _p, _p, _p, _p]
         L.oracle_splitmix64.argtypes = [_u64]
         L.oracle_splitmix64.restype = _u64
         for f in ("oracle_layout", "oracle_common_length", "oracle_pack", "oracle_unpack",
-                  "oracle_encode", "oracle_rebuild", "oracle_fill", "oracle_arc_copy", "oracle_recover"):
+                  "oracle_encode", "oracle_rebuild", "oracle_fill", "oracle_arc_copy", "oracle_recover",
+                  "oracle_aor_update", "oracle_aor_recover"):
             getattr(L, f).restype = ctypes.c_int
         _lib = L
     return _lib
@@ -204,6 +207,41 @@ def recover(scheme: int, lost, Ds, Ps, MDs, MPs, u: int):
                               ptrs[2].ctypes.data, ptrs[3].ctypes.data, Lstar, u, po.ctypes.data, pp.ctypes.data),
          "recover")
     return {j: (outD[j], outP[j]) for j in range(m) if lost[j]}
+
+
+# ---- AOR (Eq 4, P.494-505) -------------------------------
+DTYPE_BF16, DTYPE_FP32 = 1, 3
+
+
+def aor_update(w: np.ndarray, grad: np.ndarray, eta: float) -> np.ndarray:
+    """One Eq 4 step on a copy of replica ``w`` (float32): w - fp32(eta * g).
+    ``grad`` is float32, or uint16 holding bf16 bits."""
+    out = np.array(w, dtype=np.float32, copy=True)
+    g = np.ascontiguousarray(grad)
+    if g.dtype == np.float32:
+        dt = DTYPE_FP32
+    elif g.dtype == np.uint16:
+        dt = DTYPE_BF16
+    else:
+        raise OracleError("aor_update: grad must be float32 or uint16 (bf16 bits)")
+    if g.size != out.size:
+        raise OracleError("aor_update: size mismatch")
+    _chk(lib().oracle_aor_update(out.size, out.ctypes.data, g.ctypes.data, dt, ctypes.c_float(eta)), "aor_update")
+    return out
+
+
+def aor_recover(lost, masters, replicas):
+    """AOR recovery (P.505): returns (masters, replicas) after restoring the lost members.
+    ``replicas[j]`` is the replica member j holds of member (j+1) mod m."""
+    m = len(masters)
+    ms = [np.array(x, dtype=np.float32, copy=True) for x in masters]
+    rs = [np.array(x, dtype=np.float32, copy=True) for x in replicas]
+    lost_arr = np.array([1 if x else 0 for x in lost], dtype=np.uint8)
+    n = _u64arr([x.size for x in ms])
+    pm, pr = _ptrs(ms), _ptrs(rs)   # keep the pointer arrays alive across the call
+    _chk(lib().oracle_aor_recover(m, lost_arr.ctypes.data, pm.ctypes.data, pr.ctypes.data, n.ctypes.data),
+         "aor_recover")
+    return ms, rs
 
 
 # ---- generator (oracle's own copy; not part of the method) ------------------------

@@ -3,7 +3,8 @@
  *
  * Plain, slow, obviously-correct CPU oracle for REFT's snapshot-and-protect hot
  * path (arXiv 2310.12670, "REFT"): pack (snapshot image), AEC XOR parity encode,
- * single-loss rebuild (decode) and unpack (load).  Scalar byte loops only, no
+ * single-loss rebuild (decode) and unpack (load); ARC copies and two-loss recovery;
+ * AOR's Eq 4 replica update and recovery.  Scalar loops only, no
  * blocking, no vectorisation, no threads.  It shares no code, header, table or
  * constant with the CUDA path in paper_2310_12670_b200/ and neither side
  * includes the other.  Only tests/, __graft_entry__.smoke() and bench.py's
@@ -257,4 +258,63 @@ int oracle_recover(uint64_t m, uint64_t scheme, const uint8_t *lost, const uint8
         Dv[x] = outD[x];
         return oracle_encode(m, Dv, Lstar, u, x, outP[x]);
     }
+}
+
+/* ---- AOR, Asynchronous Optimizer Recomputing --------------
+ * P.494-505: under ZeRO-1 the optimizer shard of member i has no inherent redundancy,
+ * but "model parameters and gradients remain complete on each member"; each member
+ * keeps, in host memory, a replica of a peer's optimizer shard and updates it from the
+ * gradient of that shard with Eq 4 (P.502-504):
+ *     W_opt,shard^(t+1) = W_opt,shard^(t) - eta * grad W_model,shard^(t).
+ * Readings: Q22 -- fp32, index order, the product eta*g rounded to fp32
+ * before the subtraction (no fused multiply-add; SPEC S.381 "32-bit, sequential, fixed
+ * order"); a bf16 gradient is widened exactly to fp32 first.  Q23 -- ring placement as
+ * ARC: member i holds the replica of member (i+1) mod m (holder of x = (x-1) mod m). */
+
+/* One Eq 4 step of one replica: w[i] = w[i] - (eta * g[i]) for i = 0..n-1.
+ * grad_dtype: 3 = fp32 (g is float[n]), 1 = bf16 (g is uint16[n], bits << 16). */
+int oracle_aor_update(uint64_t n, float *w, const void *grad, uint64_t grad_dtype, float eta)
+{
+    uint64_t i;
+    if (n && (!w || !grad)) return ORACLE_EINVAL;
+    if (grad_dtype != 3 && grad_dtype != 1) return ORACLE_EINVAL;
+    for (i = 0; i < n; i++) {
+        float g, prod;
+        if (grad_dtype == 3) {
+            g = ((const float *)grad)[i];
+        } else {
+            union { uint32_t u; float f; } cv;
+            cv.u = (uint32_t)((const uint16_t *)grad)[i] << 16;
+            g = cv.f;
+        }
+        prod = eta * g;          /* rounded to fp32 (C99, FLT_EVAL_METHOD 0 on x86-64) */
+        w[i] = w[i] - prod;
+    }
+    return ORACLE_OK;
+}
+
+/* AOR recovery ("the system retrieves optimizer parameters from host memory with
+ * redundant parameters", P.505).  Per member j: master[j] = its optimizer shard
+ * (n[j] floats), replica[j] = the replica it holds of member (j+1) mod m (n[(j+1)%m]
+ * floats).  Lost members lost both.  Steps:
+ *   1. every lost x takes master[x] = replica[holder(x)]; a lost holder -> unrecoverable;
+ *   2. every lost x re-creates its replica: replica[x] = master[(x+1) mod m].
+ * Nothing is written when the losses are unrecoverable (m = 1 included). */
+int oracle_aor_recover(uint64_t m, const uint8_t *lost, float *const *master,
+                       float *const *replica, const uint64_t *n)
+{
+    uint64_t x, i;
+    if (m < 1 || m > 8 || !lost || !master || !replica || !n) return ORACLE_EINVAL;
+    for (x = 0; x < m; x++)
+        if (lost[x] && (m == 1 || lost[oracle_arc_holder(m, x)])) return ORACLE_EUNRECOVERABLE;
+    for (x = 0; x < m; x++) {                    /* step 1 */
+        if (!lost[x]) continue;
+        for (i = 0; i < n[x]; i++) master[x][i] = replica[oracle_arc_holder(m, x)][i];
+    }
+    for (x = 0; x < m; x++) {                    /* step 2 */
+        uint64_t o = (x + 1) % m;
+        if (!lost[x]) continue;
+        for (i = 0; i < n[o]; i++) replica[x][i] = master[o][i];
+    }
+    return ORACLE_OK;
 }

@@ -1,13 +1,20 @@
-// ckpt_lib.cu -- host side of libreft_ckpt: C ABI, planner, pinned host arena, peer
-// mapping (CUDA IPC / in-process), and the bucket pipeline scheduler.
+// ckpt_api.cu -- host side of libreft_ckpt, part 1: the C ABI entry points (errors,
+// driver memops, planner, lifecycle, register, group handshake / arena allocation,
+// HAS planner, misc).  The other units: ckpt_hostmem.cu (host memory), ckpt_pipeline.cu
+// (snapshot stages, load), ckpt_recovery.cu (rebuild / recover); shared state in
+// ckpt_internal.cuh.
 //
-// Pipeline of one snapshot, per bucket k (slot s = k mod n_slots):
-//   stream P (pack)  : [slot reuse: own D2H(k-n) done, every peer's XOR(k-n) done]
-//                      pack(k) -> READY(k) to every peer
-//   stream X (xor)   : own pack(k), every peer's READY(k), [parity slot D2H(k-n)]
-//                      xor_encode(k) over NVLink -> REL(k) to every peer
-//   stream C (copy)  : D2H data slot(k) ; D2H parity slot(k)   (copy engine, no SMs)
+// Default snapshot (n_slots = 0, full-copy staging):
+//   stream P (pack)  : one pack_all launch over every bucket; the kernel publishes
+//                      READY(k) to the local row and every peer as bucket k lands
+//   stream C (copy)  : per bucket: wait READY(k) (memop) -> D2H data(k)  (copy engine)
+//   stream X (xor)   : own pack, every peer's READY -> one xor_encode over the image
+//                      (peer reads over NVLink) -> D2H parity -> REL to every peer
 //   end              : DONE to every peer; ckpt_wait waits DONE from all, commits.
+// Slotted pipeline (n_slots > 0), per bucket k (slot s = k mod n_slots):
+//   P: [slot reuse: own D2H(k-n), peers' XOR(k-n)] pack(k) -> READY(k) to every peer
+//   X: own pack(k), peers' READY(k) -> xor_encode(k) -> REL(k) to every peer
+//   C: D2H data slot(k) ; D2H parity slot(k)
 // Cross-rank signals are 32-bit sequence numbers.  IPC groups write them into the
 // peers' flag pages with stream memory operations (cuStreamWriteValue32 /
 // cuStreamWaitValue32: zero SMs, no NCCL on the data path); LOCAL groups (all

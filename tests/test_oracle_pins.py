@@ -313,3 +313,66 @@ def test_collaborative_needs_mirrored_parity():
     stripe = (m - 1) * u
     # only bytes of unit sigma(0, 1) = 0 of each stripe of member 1 are wrong
     assert diff.size and all(d % stripe < u for d in diff)
+
+
+# ---------------------------------------------------------------- AOR (f4) ----
+# Eq 4 (PAPER.md P.502-504): W^(t+1) = W^t - eta * grad^t; reading Q22: fp32, the product
+# rounded before the subtraction; bf16 gradients widened exactly.
+def test_aor_closed_form_exact_steps():
+    # every intermediate is a dyadic rational with few bits: exact in fp32
+    w = np.array([1.0, -3.5, 0.0, 1024.0], np.float32)
+    g = np.array([0.5, -0.25, 2.0, 8.0], np.float32)
+    for t in range(1, 9):
+        w = oracle.aor_update(w, g, 0.25)
+        assert w.tolist() == [1.0 - 0.125 * t, -3.5 + 0.0625 * t, -0.5 * t, 1024.0 - 2.0 * t]
+
+
+def test_aor_product_rounded_before_subtraction():
+    # eta = g = 1 + 2^-12: eta*g = 1 + 2^-11 + 2^-24 rounds (tie to even) to 1 + 2^-11,
+    # so w = 1 + 2^-11 gives exactly 0; a fused multiply-add would give -2^-24.
+    x = np.float32(1.0 + 2.0**-12)
+    w = np.array([1.0 + 2.0**-11], np.float32)
+    out = oracle.aor_update(w, np.array([x], np.float32), float(x))
+    assert out[0] == 0.0 and not np.signbit(out[0])
+
+
+def test_aor_matches_numpy_float32_per_op():
+    rng = np.random.default_rng(7)
+    w = rng.standard_normal(4099).astype(np.float32)
+    g = (rng.standard_normal(4099) * 1e-3).astype(np.float32)
+    for eta in (1e-3, 0.1, 3.0e-4, 1.0):
+        e32 = np.float32(eta)
+        want = w - (e32 * g)          # numpy float32 ops: each rounded to fp32
+        assert np.array_equal(oracle.aor_update(w, g, eta).view(np.uint32), want.view(np.uint32))
+
+
+def test_aor_bf16_gradient_widening():
+    import torch
+    bits = np.array([0x3F80, 0xC000, 0x4049, 0x0000, 0x8000, 0x0001, 0x7F7F, 0x3C23, 0xBE4D], np.uint16)
+    # bf16 -> fp32 through torch's own conversion (an independent library routine)
+    gf = torch.from_numpy(bits.view(np.int16).copy()).view(torch.bfloat16).float().numpy()
+    assert gf[:3].tolist() == [1.0, -2.0, 3.140625]
+    w = np.linspace(-2, 2, bits.size).astype(np.float32)
+    for eta in (0.5, 1e-3):
+        assert np.array_equal(oracle.aor_update(w, bits, eta).view(np.uint32),
+                              oracle.aor_update(w, gf.astype(np.float32), eta).view(np.uint32))
+
+
+@pytest.mark.parametrize("m", [1, 2, 3, 4, 5])
+def test_aor_recover_brute_force_masks(m):
+    rng = np.random.default_rng(m)
+    sizes = [int(rng.integers(0, 9)) for _ in range(m)]
+    masters0 = [rng.standard_normal(n).astype(np.float32) for n in sizes]
+    replicas0 = [masters0[(j + 1) % m].copy() for j in range(m)]   # ring: j holds j+1 (SPEC S.313)
+    for mask in range(1, 1 << m):
+        lost = [(mask >> j) & 1 for j in range(m)]
+        ms = [np.full(sizes[j], np.nan, np.float32) if lost[j] else masters0[j] for j in range(m)]
+        rs = [np.full(sizes[(j + 1) % m], np.nan, np.float32) if lost[j] else replicas0[j] for j in range(m)]
+        adjacent = any(lost[j] and lost[(j - 1) % m] for j in range(m))
+        if m == 1 or adjacent:
+            with pytest.raises(oracle.OracleError, match="unrecoverable"):
+                oracle.aor_recover(lost, ms, rs)
+            continue
+        got_m, got_r = oracle.aor_recover(lost, ms, rs)
+        for j in range(m):
+            assert np.array_equal(got_m[j], masters0[j]) and np.array_equal(got_r[j], replicas0[j])
