@@ -1,6 +1,6 @@
 """Build the in-tree CUDA libraries for sm_100a with nvcc (no JIT, no torch ext).
 
-  libreft_ckpt.so  -- the product: C ABI of include/ckpt.h
+  libreft_ckpt.so  -- the product: C ABI of include/ckpt.h and include/ckpt_aor.h
   libreft_synth.so -- harness: seeded GPU generator of include/reft_synth.h
 
 Both link the CUDA runtime statically; the driver API entry points (stream memory
@@ -17,11 +17,12 @@ ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
-FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O2,-Wall,-fvisibility=hidden", "-shared",
+FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O2,-Wall,-fvisibility=hidden,-ffp-contract=off", "-shared",
          "-Xptxas", "-v", "-I" + os.path.join(ROOT, "include")]
 
 LIBS = {
-    "libreft_ckpt.so": ["ckpt_api.cu", "ckpt_hostmem.cu", "ckpt_pipeline.cu", "ckpt_recovery.cu", "ckpt_kernels.cu"],
+    "libreft_ckpt.so": ["ckpt_api.cu", "ckpt_hostmem.cu", "ckpt_pipeline.cu", "ckpt_recovery.cu", "ckpt_kernels.cu",
+                        "ckpt_aor.cu", "aor_update.cpp"],
     "libreft_synth.so": ["synth_fill.cu"],
 }
 
@@ -31,7 +32,7 @@ def _stale(out, srcs):
         return True
     t = os.path.getmtime(out)
     deps = srcs + [os.path.join(CSRC, "ckpt_kernels.cuh"), os.path.join(CSRC, "ckpt_internal.cuh"),
-                   os.path.join(ROOT, "include", "ckpt.h"),
+                   os.path.join(ROOT, "include", "ckpt.h"), os.path.join(ROOT, "include", "ckpt_aor.h"),
                    os.path.join(ROOT, "include", "reft_synth.h")]
     return any(os.path.getmtime(d) > t for d in deps)
 

@@ -90,6 +90,24 @@ class ckpt_has_plan_t(ctypes.Structure):
                 ("compute_bytes", _u64)]
 
 
+CKPT_AOR_PERSIST = 0x1
+CKPT_AOR_EMPTY, CKPT_AOR_CLEAN, CKPT_AOR_UPDATING, CKPT_AOR_POISONED, CKPT_AOR_SEEDING = 0, 1, 2, 3, 4
+
+
+class ckpt_aor_options(ctypes.Structure):
+    _fields_ = [("struct_size", _u32), ("grad_dtype", _u32), ("chunk_bytes", _u64), ("n_slots", _u32),
+                ("threads", _u32), ("priority", _i32), ("flags", _u32), ("key", _u64), ("reserved", _u32 * 4)]
+
+
+class ckpt_aor_shard(ctypes.Structure):
+    _fields_ = [("master", _vp), ("grad", _vp), ("bounds", ctypes.POINTER(_u64)), ("m", _u32), ("my_index", _u32)]
+
+
+class ckpt_aor_stats(ctypes.Structure):
+    _fields_ = [(n, _u64) for n in ("steps", "chunks", "d2h_bytes", "h2d_bytes")] + \
+               [(n, ctypes.c_double) for n in ("update_s", "stall_s", "last_step_ms")]
+
+
 class CkptError(RuntimeError):
     def __init__(self, code: int, where: str, msg: str):
         self.code = code
@@ -138,6 +156,22 @@ def lib():
             "ckpt_plan_common": (ctypes.c_int, [_vp, _u32, _u64, ctypes.POINTER(_u64), ctypes.POINTER(_u64)]),
             "ckpt_version": (ctypes.c_char_p, []),
             "ckpt_arena_unlink": (ctypes.c_int, [_u64, _u32, _u32]),
+            # include/ckpt_aor.h
+            "ckpt_aor_options_default": (None, [ctypes.POINTER(ckpt_aor_options)]),
+            "ckpt_aor_create": (ctypes.c_int, [ctypes.c_int, ctypes.POINTER(ckpt_aor_options),
+                                               ctypes.POINTER(ckpt_aor_shard), ctypes.POINTER(_vp)]),
+            "ckpt_aor_destroy": (ctypes.c_int, [_vp]),
+            "ckpt_aor_seed": (ctypes.c_int, [_vp, _u64, _vp]),
+            "ckpt_aor_step": (ctypes.c_int, [_vp, ctypes.c_float, _vp, ctypes.POINTER(_u64)]),
+            "ckpt_aor_fence": (ctypes.c_int, [_vp, _u64, _vp]),
+            "ckpt_aor_wait": (ctypes.c_int, [_vp, _u64]),
+            "ckpt_aor_restore": (ctypes.c_int, [_vp, _vp, ctypes.POINTER(_u64)]),
+            "ckpt_aor_forget": (ctypes.c_int, [_vp, ctypes.c_uint8]),
+            "ckpt_aor_view": (ctypes.c_int, [_vp, ctypes.POINTER(_vp), ctypes.POINTER(_u64), ctypes.POINTER(_u64),
+                                             ctypes.POINTER(_u32)]),
+            "ckpt_aor_get_stats": (ctypes.c_int, [_vp, ctypes.POINTER(ckpt_aor_stats)]),
+            "ckpt_aor_unlink": (ctypes.c_int, [_u64, _u32]),
+            "ckpt_aor_apply": (ctypes.c_int, [_vp, _vp, _u32, _u64, ctypes.c_float]),
         }
         for name, (res, args) in sig.items():
             f = getattr(L, name)
@@ -401,3 +435,130 @@ def reft_synth_fill(ptr: int, nbytes: int, seed: int, rank: int, tensor: int, xo
     rc = _synth.reft_synth_fill(ptr, nbytes, seed, rank, tensor, xor_mode, _stream_handle(stream))
     if rc != 0:
         raise RuntimeError(f"reft_synth_fill failed ({rc})")
+
+
+# ---------------------------------------------------------------- AOR (include/ckpt_aor.h) ----
+def ckpt_aor_options_default(**kw) -> ckpt_aor_options:
+    o = ckpt_aor_options()
+    lib().ckpt_aor_options_default(ctypes.byref(o))
+    for k, v in kw.items():
+        setattr(o, k, v)
+    return o
+
+
+def ckpt_aor_create(device: int, options: ckpt_aor_options, master, grad, bounds: Sequence[int],
+                    my_index: int) -> int:
+    """master: this member's fp32 optimizer shard (device tensor or pointer); grad: the complete
+    flat gradient (device tensor or pointer); bounds: m+1 element offsets of the partition."""
+    b = (_u64 * len(bounds))(*[int(x) for x in bounds])
+    sh = ckpt_aor_shard(_ptr(master), _ptr(grad), ctypes.cast(b, ctypes.POINTER(_u64)), len(bounds) - 1, my_index)
+    a = _vp()
+    _check(lib().ckpt_aor_create(device, ctypes.byref(options), ctypes.byref(sh), ctypes.byref(a)), "ckpt_aor_create")
+    return a.value
+
+
+def _ptr(x) -> int:
+    if x is None:
+        return 0
+    if isinstance(x, int):
+        return x
+    return x.data_ptr() if x.numel() else 0
+
+
+def ckpt_aor_destroy(a: int) -> None:
+    _check(lib().ckpt_aor_destroy(a), "ckpt_aor_destroy")
+
+
+def ckpt_aor_seed(a: int, step: int = 0, stream=None) -> None:
+    _check(lib().ckpt_aor_seed(a, step, _stream_handle(stream)), "ckpt_aor_seed")
+
+
+def ckpt_aor_step(a: int, eta: float, stream=None) -> int:
+    t = _u64()
+    _check(lib().ckpt_aor_step(a, eta, _stream_handle(stream), ctypes.byref(t)), "ckpt_aor_step")
+    return t.value
+
+
+def ckpt_aor_fence(a: int, step: int, stream=None) -> None:
+    _check(lib().ckpt_aor_fence(a, step, _stream_handle(stream)), "ckpt_aor_fence")
+
+
+def ckpt_aor_wait(a: int, step: int) -> None:
+    _check(lib().ckpt_aor_wait(a, step), "ckpt_aor_wait")
+
+
+def ckpt_aor_restore(a: int, stream=None) -> int:
+    t = _u64()
+    _check(lib().ckpt_aor_restore(a, _stream_handle(stream), ctypes.byref(t)), "ckpt_aor_restore")
+    return t.value
+
+
+def ckpt_aor_forget(a: int, poison: int = 0xA5) -> None:
+    _check(lib().ckpt_aor_forget(a, poison), "ckpt_aor_forget")
+
+
+def ckpt_aor_view(a: int, copy: bool = True):
+    """(replica float32 array, step, state) of the replica this member holds."""
+    p, n, t, st = _vp(), _u64(), _u64(), _u32()
+    _check(lib().ckpt_aor_view(a, ctypes.byref(p), ctypes.byref(n), ctypes.byref(t), ctypes.byref(st)),
+           "ckpt_aor_view")
+    if n.value == 0:
+        arr = np.zeros(0, np.float32)
+    else:
+        arr = np.ctypeslib.as_array((ctypes.c_float * n.value).from_address(p.value))
+        if copy:
+            arr = arr.copy()
+    return arr, t.value, st.value
+
+
+def ckpt_aor_get_stats(a: int) -> dict:
+    s = ckpt_aor_stats()
+    _check(lib().ckpt_aor_get_stats(a, ctypes.byref(s)), "ckpt_aor_get_stats")
+    return {n: getattr(s, n) for n, _ in s._fields_}
+
+
+def ckpt_aor_unlink(key: int, m: int) -> None:
+    _check(lib().ckpt_aor_unlink(key, m), "ckpt_aor_unlink")
+
+
+def ckpt_aor_apply(w: np.ndarray, grad: np.ndarray, eta: float) -> None:
+    """Host-only: one Eq 4 step in place on float32 ``w`` (grad float32, or uint16 bf16 bits)."""
+    assert w.dtype == np.float32 and w.flags.c_contiguous and grad.flags.c_contiguous and grad.size == w.size
+    dt = CKPT_DTYPE_BF16 if grad.dtype == np.uint16 else CKPT_DTYPE_FP32
+    assert grad.dtype in (np.uint16, np.float32)
+    _check(lib().ckpt_aor_apply(w.ctypes.data, grad.ctypes.data, dt, w.size, eta), "ckpt_aor_apply")
+
+
+def aor_group_key(group=None) -> int:
+    """A random non-zero key chosen by rank 0 of ``group`` and broadcast (torch.distributed)."""
+    import torch
+    import torch.distributed as dist
+    key = int.from_bytes(os.urandom(8), "little") | 1
+    if dist.is_available() and dist.is_initialized() and dist.get_world_size(group) > 1:
+        dev = torch.device("cuda", torch.cuda.current_device()) if dist.get_backend(group) == "nccl" else "cpu"
+        t = torch.tensor([key & 0x7FFFFFFFFFFFFFFF], dtype=torch.int64, device=dev)
+        dist.broadcast(t, src=dist.get_global_rank(group, 0) if group is not None else 0, group=group)
+        key = int(t.item())
+    return key
+
+
+def aor_recover(a: int, lost_mask: int, my_index: int, m: int, barrier, stream=None) -> int:
+    """The recovery protocol of include/ckpt_aor.h over a group barrier (e.g. dist.barrier):
+    survivors drain, lost members restore their master shard from their holder, and the
+    owners of the replicas the lost members held re-seed them.  Every member calls this with
+    the same lost_mask; returns the step of the restored state (-1 on members that restored
+    nothing and seeded nothing)."""
+    lost = [(lost_mask >> j) & 1 for j in range(m)]
+    if any(lost[j] and lost[(j - 1) % m] for j in range(m)) or (m == 1 and lost[0]):
+        raise CkptError(CKPT_EUNRECOVERABLE, "aor_recover", "a lost member's holder is lost too")
+    step = -1
+    if not lost[my_index]:
+        _, step, _ = ckpt_aor_view(a, copy=False)    # drains this member's pending updates
+    barrier()
+    if lost[my_index]:
+        step = ckpt_aor_restore(a, stream)
+    barrier()
+    if lost[(my_index - 1) % m] and not lost[my_index]:
+        ckpt_aor_seed(a, step, stream)   # this member's master is at the group's step
+    barrier()
+    return step

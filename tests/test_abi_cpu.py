@@ -31,6 +31,10 @@ def test_every_declared_symbol_is_exported(C):
     assert len(names) >= 20
     for n in names:
         assert hasattr(lib, n), f"libreft_ckpt.so does not export {n}"
+    aor = declared("ckpt_aor.h")
+    assert len(aor) >= 12
+    for n in aor:
+        assert hasattr(lib, n), f"libreft_ckpt.so does not export {n}"
     synth = ctypes.CDLL(C.SYNTH_PATH)
     for n in declared("reft_synth.h"):
         assert hasattr(synth, n), n
@@ -108,3 +112,63 @@ def test_has_plan_spec_vectors(C):
     assert (p["bubble_bytes"], p["compute_bytes"]) == (0, 100)
     with pytest.raises(C.CkptError):
         C.ckpt_has_plan(4, 4, 1.0, 1, 1.0)
+
+
+# ---------------------------------------------------------------- AOR host arithmetic ----
+@pytest.mark.parametrize("bf16", [False, True])
+def test_aor_host_update_matches_oracle(C, bf16):
+    """The library's Eq 4 routine (the one its worker threads run) vs the oracle, bit for bit,
+    over ragged lengths that exercise the AVX-512 body and the scalar tail."""
+    rng = np.random.default_rng(11)
+    for n in (0, 1, 15, 16, 17, 31, 33, 1000, 65_537):
+        w = rng.standard_normal(n).astype(np.float32)
+        if bf16:
+            g = (rng.standard_normal(n).astype(np.float32).view(np.uint32) >> 16).astype(np.uint16)
+        else:
+            g = (rng.standard_normal(n) * 1e-2).astype(np.float32)
+        for eta in (1e-3, 0.37, 1.0):
+            got = w.copy()
+            C.ckpt_aor_apply(got, g, eta)
+            assert np.array_equal(got.view(np.uint32), oracle.aor_update(w, g, eta).view(np.uint32)), (n, eta)
+
+
+def test_aor_host_update_has_no_fma():
+    """Reading Q22 (product rounded before the subtraction): no fused multiply-add in the
+    library's host update routines (build.py passes -ffp-contract=off)."""
+    import subprocess
+    from paper_2310_12670_b200 import build
+    so = build.build()["libreft_ckpt.so"]
+    dis = subprocess.run(["objdump", "-d", "--no-show-raw-insn", so], capture_output=True, text=True).stdout
+    body, cur = {}, None
+    for line in dis.splitlines():
+        if line.endswith(">:"):
+            cur = line if "sgd" in line else None
+            if cur:
+                body[cur] = []
+        elif not line.strip():
+            cur = None
+        elif cur:
+            body[cur].append(line)
+    assert len(body) >= 3 and any("aor_sgd" in k for k in body), "update routines not found"
+    insns = "\n".join("\n".join(v) for v in body.values())
+    assert "vmulps" in insns and "vsubps" in insns
+    assert not re.search(r"\bv?f(n)?m(add|sub)", insns), "FMA found in the Eq 4 routines"
+
+
+def test_aor_no_gpu_means_error(C):
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    o = C.ckpt_aor_options_default(key=12345)
+    with pytest.raises(C.CkptError) as e:
+        C.ckpt_aor_create(0, o, 0x1000, 0x2000, [0, 10, 20], 0)
+    assert e.value.code == C.CKPT_ECUDA
+
+
+def test_aor_options_and_protocol_guard(C):
+    o = C.ckpt_aor_options_default()
+    assert (o.grad_dtype, o.chunk_bytes, o.n_slots, o.key) == (C.CKPT_DTYPE_FP32, 16 << 20, 0, 0)
+    # adjacent losses are refused before any barrier or call (oracle_aor_recover's rule)
+    with pytest.raises(C.CkptError) as e:
+        C.aor_recover(0, 0b0110, 1, 4, barrier=lambda: None)
+    assert e.value.code == C.CKPT_EUNRECOVERABLE
