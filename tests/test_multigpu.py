@@ -433,3 +433,123 @@ def test_ipc_disjoint_subgroups():
                 p.kill()
     for rank, ok, _ in res:
         assert all(ok), (rank, ok)
+
+
+# ---------------------------------------------------------------- AOR (f4) --------------
+def _aor_worker(rank, world, port, q):
+    """ZeRO-1 members, one process per GPU: Eq 4 replicas vs the oracle and vs the owners'
+    device shards; then every member in turn is lost (device shard + held replica, context
+    re-created) and recovered with the protocol of include/ckpt_aor.h over dist.barrier."""
+    try:
+        os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank), WORLD_SIZE=str(world))
+        import torch
+        import torch.distributed as dist
+
+        import oracle
+        from paper_2310_12670_b200 import ckpt as C
+
+        torch.cuda.set_device(rank)
+        dev = torch.device("cuda", rank)
+        dist.init_process_group("nccl", device_id=dev)
+        sizes = [70_003 + 9_001 * j for j in range(world)]
+        bounds = [0]
+        for n in sizes:
+            bounds.append(bounds[-1] + n)
+        owner = (rank + 1) % world
+        gen = torch.Generator(device=dev).manual_seed(5)       # the all-reduced gradient: same everywhere
+        master = torch.randn(sizes[rank], device=dev, generator=torch.Generator(device=dev).manual_seed(100 + rank))
+        grad = torch.empty(bounds[-1], device=dev)
+        key = C.aor_group_key()
+        opt = C.ckpt_aor_options_default(key=key, chunk_bytes=64 << 10, n_slots=2, flags=C.CKPT_AOR_PERSIST)
+        a = C.ckpt_aor_create(rank, opt, master, grad, bounds, rank)
+        dist.barrier()
+        C.ckpt_aor_seed(a, 0)
+        dist.barrier()
+        rep = C.ckpt_aor_view(a)[0]
+        t = 0
+
+        def steps(n):
+            nonlocal rep, t
+            for _ in range(n):
+                eta = 0.01 * (t + 1)
+                grad.copy_(torch.randn(bounds[-1], device=dev, generator=gen) * 1e-2)
+                s = C.ckpt_aor_step(a, eta)
+                C.ckpt_aor_fence(a, s)
+                rep = oracle.aor_update(rep, grad[bounds[owner]:bounds[owner + 1]].cpu().numpy(), eta)
+                master.sub_(grad[bounds[rank]:bounds[rank + 1]] * eta)
+                grad.fill_(float("nan"))
+                t += 1
+
+        def check():
+            got, step, state = C.ckpt_aor_view(a)
+            masters = [None] * world
+            dist.all_gather_object(masters, master.cpu().numpy())
+            return (state == C.CKPT_AOR_CLEAN and step == t
+                    and np.array_equal(got.view(np.uint32), rep.view(np.uint32))
+                    and np.array_equal(got.view(np.uint32), masters[owner].view(np.uint32))), masters
+
+        ok = []
+        steps(3)
+        good, masters = check()
+        ok.append(good)
+        for x in range(world):
+            if rank == x:
+                master.view(torch.int32).fill_(0x7FA5A5A5)
+                C.ckpt_aor_forget(a)
+                C.ckpt_aor_destroy(a)
+                a = C.ckpt_aor_create(rank, opt, master, grad, bounds, rank)   # the replacement re-attaches
+            dist.barrier()
+            step = C.aor_recover(a, 1 << x, rank, world, dist.barrier)
+            torch.cuda.synchronize()
+            ok.append(step == t)
+            ok.append(bool(np.array_equal(master.cpu().numpy().view(np.uint32), masters[rank].view(np.uint32))))
+            if rank == x:
+                rep = masters[owner].copy()        # its held replica was re-seeded by its owner
+            steps(1)
+            good, masters = check()
+            ok.append(good)
+        C.ckpt_aor_destroy(a)
+        dist.barrier()
+        if rank == 0:
+            C.ckpt_aor_unlink(key, world)
+        dist.destroy_process_group()
+        q.put((rank, ok, None))
+    except Exception:
+        q.put((rank, None, traceback.format_exc()))
+
+
+def _run_fn(fn, world, timeout=300):
+    import queue
+    import time
+
+    import torch.multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    os.environ.setdefault("CKPT_TIMEOUT_S", "90")
+    ps = [ctx.Process(target=fn, args=(r, world, port, q)) for r in range(world)]
+    for p in ps:
+        p.start()
+    res, t0 = [], time.time()
+    try:
+        while len(res) < world:
+            try:
+                r = q.get(timeout=5)
+            except queue.Empty:
+                dead = [p for p in ps if p.exitcode not in (None, 0)]
+                assert not dead, f"worker died: exit codes {[p.exitcode for p in ps]}"
+                assert time.time() - t0 < timeout, "multi-GPU case timed out"
+                continue
+            res.append(r)
+            assert r[2] is None, f"rank {r[0]}:\n{r[2]}"
+    finally:
+        for p in ps:
+            p.join(30 if len(res) == world else 1)
+            if p.is_alive():
+                p.kill()
+    for rank, ok, err in sorted(res, key=lambda x: x[0]):
+        assert all(ok), f"rank {rank}: {ok}"
+
+
+def test_aor_zero1_members_all_gpus():
+    _run_fn(_aor_worker, min(_world(), 8))

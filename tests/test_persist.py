@@ -174,3 +174,97 @@ def test_restart_after_host_memory_loss(built, m, scheme, drop):
             assert np.array_equal(np.frombuffer(b, np.uint8), want[(j, t)]), (j, t)
     finally:
         C.ckpt_arena_unlink(key, m, 2)
+
+
+# ---------------------------------------------------------------- AOR (f4) ----------------
+# The replica objects are shared memory too: after every member's process died, a restarted
+# process re-attaches them (same key) and every member restores its optimizer shard from its
+# holder's replica -- exactly the owners' state at the replica's step, or, for a replica an
+# update was torn in (the process died inside Eq 4), a refusal.
+AOR_SIZES = [60_001, 1_234, 200_000]
+
+
+def _aor_child(key, phase, q):
+    try:
+        import torch
+
+        from paper_2310_12670_b200 import ckpt as C
+        m = len(AOR_SIZES)
+        bounds = [0]
+        for n in AOR_SIZES:
+            bounds.append(bounds[-1] + n)
+        gen = torch.Generator(device="cuda").manual_seed(3)
+        masters = [torch.randn(n, device="cuda", generator=gen) for n in AOR_SIZES]
+        grad = torch.empty(bounds[-1], device="cuda")
+        opt = C.ckpt_aor_options_default(key=key, chunk_bytes=64 << 10, flags=C.CKPT_AOR_PERSIST)
+        ctx = [C.ckpt_aor_create(0, opt, masters[j], grad, bounds, j) for j in range(m)]
+        for a in ctx:
+            C.ckpt_aor_seed(a, 0)
+        out = {}
+        for t in range(1, 4 if phase == "mid" else 3):
+            eta = 0.05 * t
+            grad.copy_(torch.randn(bounds[-1], device="cuda", generator=gen) * 1e-2)
+            ids = [C.ckpt_aor_step(a, eta) for a in ctx]
+            for a, s in zip(ctx, ids):
+                C.ckpt_aor_fence(a, s)
+            for j in range(m):
+                masters[j].sub_(grad[bounds[j]:bounds[j + 1]] * eta)
+            out[t] = [x.cpu().numpy().tobytes() for x in masters]
+            if t <= 2:
+                for a, s in zip(ctx, ids):
+                    C.ckpt_aor_wait(a, s)
+        q.put(("ok", out))
+        q.close()
+        q.join_thread()
+        os._exit(0)                          # no destroy: the objects stay (persistent)
+    except Exception:
+        q.put(("err", traceback.format_exc()))
+        q.close()
+        q.join_thread()
+        os._exit(1)
+
+
+def _aor_reader(key, q):
+    try:
+        import torch
+
+        from paper_2310_12670_b200 import ckpt as C
+        m = len(AOR_SIZES)
+        bounds = [0]
+        for n in AOR_SIZES:
+            bounds.append(bounds[-1] + n)
+        masters = [torch.full((n,), float("nan"), device="cuda") for n in AOR_SIZES]
+        grad = torch.zeros(bounds[-1], device="cuda")
+        opt = C.ckpt_aor_options_default(key=key, chunk_bytes=64 << 10, flags=C.CKPT_AOR_PERSIST)
+        ctx = [C.ckpt_aor_create(0, opt, masters[j], grad, bounds, j) for j in range(m)]
+        res = []
+        for j in range(m):
+            try:
+                step = C.ckpt_aor_restore(ctx[j])
+                torch.cuda.synchronize()
+                res.append((j, step, masters[j].cpu().numpy().tobytes()))
+            except C.CkptError as e:
+                held = ctx[(j - 1) % m]
+                res.append((j, e.code, C.ckpt_aor_view(held)[2]))
+        for a in ctx:
+            C.ckpt_aor_destroy(a)
+        q.put(("ok", res))
+    except Exception:
+        q.put(("err", traceback.format_exc()))
+
+
+@pytest.mark.parametrize("phase", ["clean", "mid"])
+def test_aor_replicas_survive_process_death(built, phase):
+    from paper_2310_12670_b200 import ckpt as C
+    key = int.from_bytes(os.urandom(8), "little") | 1
+    try:
+        want = _run(_aor_child, key, phase)
+        got = _run(_aor_reader, key)
+        for j, a, b in got:
+            if phase == "clean" or a in (2, 3) and isinstance(b, bytes):
+                assert a == 2 if phase == "clean" else a in (2, 3), (j, a)
+                assert b == want[a][j], f"member {j}: restored shard differs from the owner's at step {a}"
+            else:                             # a torn replica (Eq 4 was running) is refused
+                assert a == C.CKPT_EUNRECOVERABLE and b == C.CKPT_AOR_UPDATING, (j, a, b)
+    finally:
+        C.ckpt_aor_unlink(key, len(AOR_SIZES))
