@@ -582,6 +582,107 @@ __global__ void __launch_bounds__(kXorThreads) xor_kernel(const XorArgs a) {
 template <int N>
 constexpr int xor_unroll() { return N == 1 ? 8 : N == 2 ? 4 : N == 3 ? 3 : 2; }
 
+// ---------------------------------------------------------------------------------
+// TMA XOR gather.  Same contract as xor_kernel.  W warps per CTA (one CTA per SM), each an
+// independent pipeline over tiles of T bytes of one unit: lane 0 loads the NIN input
+// segments of a tile with cp.async.bulk (peer staging over NVLink for the encode; an
+// mbarrier counts the bytes) into one of NS SMEM stages, the 32 lanes XOR the segments out
+// of SMEM and store the result with 128-bit stores.  Each warp keeps NS tiles = NS*NIN*T
+// bytes of peer reads in flight (~48 KiB, ~190 KiB per SM) with one instruction per
+// segment instead of one per 16 B.  Segments past an input's `valid` are not loaded and
+// read as zero (reading Q5).
+template <int NIN>
+struct XorTmaCfg {  // T * NIN * NS <= 48 KiB per warp, NS >= 3
+    static constexpr uint32_t T = NIN == 1 ? 16384 : NIN == 2 ? 8192 : NIN <= 4 ? 4096 : 2048;
+    static constexpr int NS = (int)((48u * 1024u) / (T * NIN)) > 6 ? 6 : (int)((48u * 1024u) / (T * NIN));
+    static constexpr int W = 4;
+    static constexpr int smem = W * NS * NIN * (int)T;
+};
+
+template <int NIN>
+__device__ __forceinline__ void xor_tile_geometry(const XorArgs &a, uint64_t t, uint64_t tpu, uint32_t T,
+                                                  uint64_t &s, uint64_t &uoff, uint32_t &len, uint32_t (&n)[NIN],
+                                                  uint64_t (&pos)[NIN]) {
+    s = t / tpu;
+    uoff = (t - s * tpu) * T;
+    len = (uint32_t)((a.unit - uoff) < T ? (a.unit - uoff) : T);
+#pragma unroll
+    for (int k = 0; k < NIN; ++k) {
+        pos[k] = s * a.in[k].stride + a.in[k].off + uoff;
+        const uint64_t v = a.in[k].valid;
+        n[k] = pos[k] >= v ? 0u : (uint32_t)((v - pos[k]) < len ? (v - pos[k]) : len);
+    }
+}
+
+template <int NIN>
+__global__ void __launch_bounds__(32 * XorTmaCfg<NIN>::W) xor_tma_kernel(const __grid_constant__ XorArgs a) {
+    using Cfg = XorTmaCfg<NIN>;
+    constexpr uint32_t T = Cfg::T;
+    constexpr int NS = Cfg::NS, W = Cfg::W;
+    extern __shared__ __align__(128) uint8_t smem[];
+    __shared__ __align__(8) uint64_t bars[W][NS];
+    const uint32_t lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    uint8_t *ring = smem + (size_t)w * NS * NIN * T;
+    if (lane == 0) {
+        for (int i = 0; i < NS; ++i) mbar_init(&bars[w][i], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    }
+    __syncwarp();
+    const uint64_t tpu = (a.unit + T - 1) / T;
+    const uint64_t ntiles = a.nstripes * tpu;
+    const uint64_t step = (uint64_t)gridDim.x * W;
+    auto issue = [&](uint64_t t, int st) {  // lane 0 only
+        uint64_t s, uoff;
+        uint32_t len, n[NIN];
+        uint64_t pos[NIN];
+        xor_tile_geometry<NIN>(a, t, tpu, T, s, uoff, len, n, pos);
+        uint32_t total = 0;
+#pragma unroll
+        for (int k = 0; k < NIN; ++k) total += n[k];
+        mbar_expect_tx(&bars[w][st], total);  // total = 0 completes the phase at once
+#pragma unroll
+        for (int k = 0; k < NIN; ++k)
+            if (n[k]) bulk_g2s(ring + ((size_t)st * NIN + k) * T, a.in[k].base + pos[k], n[k], &bars[w][st]);
+    };
+    uint64_t t_issue = (uint64_t)blockIdx.x * W + w, t = t_issue;
+    if (lane == 0)
+        for (int i = 0; i < NS && t_issue < ntiles; ++i, t_issue += step) issue(t_issue, i);
+    t_issue = t + (uint64_t)NS * step;  // every lane tracks the issue cursor
+    uint32_t phase = 0;
+    for (int st = 0; t < ntiles; t += step, st = (st + 1 == NS) ? 0 : st + 1) {
+        uint64_t s, uoff;
+        uint32_t len, n[NIN];
+        uint64_t pos[NIN];
+        xor_tile_geometry<NIN>(a, t, tpu, T, s, uoff, len, n, pos);
+        mbar_wait(&bars[w][st], (phase >> st) & 1);
+        phase ^= 1u << st;
+        const uint4 *seg = reinterpret_cast<const uint4 *>(ring + (size_t)st * NIN * T);
+        const uint64_t obase = s * a.out_stride + a.out_off + uoff;
+        for (uint32_t i = lane; i < (len >> 4); i += 32) {
+            uint4 acc = make_uint4(0, 0, 0, 0);
+#pragma unroll
+            for (int k = 0; k < NIN; ++k) {
+                if ((i << 4) < n[k]) {
+                    const uint4 v = seg[(size_t)k * (T >> 4) + i];
+                    acc.x ^= v.x;
+                    acc.y ^= v.y;
+                    acc.z ^= v.z;
+                    acc.w ^= v.w;
+                }
+            }
+            const uint64_t o = obase + ((uint64_t)i << 4);
+            if (o < a.out_valid) *reinterpret_cast<uint4 *>(a.out + o) = acc;
+        }
+        __syncwarp();  // every lane is done reading stage st
+        if (lane == 0 && t_issue < ntiles) {
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            issue(t_issue, st);
+        }
+        t_issue += step;
+    }
+}
+
 template <int N>
 cudaError_t launch_xor_n(const XorArgs &a, int max_ctas, cudaStream_t s) {
     constexpr int U = xor_unroll<N>();
@@ -590,6 +691,24 @@ cudaError_t launch_xor_n(const XorArgs &a, int max_ctas, cudaStream_t s) {
     const uint64_t ntiles = a.nstripes * tpu;
     const int grid = (int)(ntiles < (uint64_t)max_ctas ? ntiles : (uint64_t)max_ctas);
     xor_kernel<N, U><<<grid, kXorThreads, 0, s>>>(a);
+    return cudaGetLastError();
+}
+
+template <int N>
+cudaError_t launch_xor_tma_n(const XorArgs &a, int ctas, cudaStream_t s) {
+    using Cfg = XorTmaCfg<N>;
+    static unsigned long long attr_set = 0;  // bit d: attribute set on device d
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (!(attr_set & (1ull << dev))) {
+        cudaError_t e = cudaFuncSetAttribute(xor_tma_kernel<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::smem);
+        if (e != cudaSuccess) return e;
+        attr_set |= 1ull << dev;
+    }
+    const uint64_t ntiles = a.nstripes * ((a.unit + Cfg::T - 1) / Cfg::T);
+    const uint64_t need = (ntiles + Cfg::W - 1) / Cfg::W;
+    const int grid = (int)(need < (uint64_t)ctas ? need : (uint64_t)ctas);
+    xor_tma_kernel<N><<<grid, 32 * Cfg::W, Cfg::smem, s>>>(a);
     return cudaGetLastError();
 }
 
@@ -651,6 +770,9 @@ cudaError_t preload_kernels() {
         (const void *)xor_kernel<3, xor_unroll<3>()>, (const void *)xor_kernel<4, xor_unroll<4>()>,
         (const void *)xor_kernel<5, xor_unroll<5>()>, (const void *)xor_kernel<6, xor_unroll<6>()>,
         (const void *)xor_kernel<7, xor_unroll<7>()>, (const void *)xor_kernel<8, xor_unroll<8>()>,
+        (const void *)xor_tma_kernel<1>, (const void *)xor_tma_kernel<2>, (const void *)xor_tma_kernel<3>,
+        (const void *)xor_tma_kernel<4>, (const void *)xor_tma_kernel<5>, (const void *)xor_tma_kernel<6>,
+        (const void *)xor_tma_kernel<7>, (const void *)xor_tma_kernel<8>,
         (const void *)signal_kernel};
     for (const void *f : fns) {
         cudaError_t e = cudaFuncGetAttributes(&fa, f);
@@ -696,6 +818,28 @@ cudaError_t launch_xor(const XorArgs &a, int max_ctas, cudaStream_t s) {
         cap = e ? std::max(0, atoi(e)) : 0;
     }
     if (cap > 0) max_ctas = cap;
+    static int impl = -1;  // CKPT_XOR_IMPL: tma (default) | lsu
+    if (impl < 0) {
+        const char *e = getenv("CKPT_XOR_IMPL");
+        impl = (e && !strcmp(e, "lsu")) ? 0 : 1;
+    }
+    bool aligned = ((uintptr_t)a.out & 15) == 0 && (a.out_stride & 15) == 0 && (a.out_off & 15) == 0;
+    for (int k = 0; k < a.nin; ++k)
+        aligned = aligned && ((uintptr_t)a.in[k].base & 15) == 0 && (a.in[k].stride & 15) == 0 &&
+                  (a.in[k].off & 15) == 0 && (a.in[k].valid & 15) == 0;
+    if (impl == 1 && aligned) {
+        const int ctas = max_ctas / 2 > 0 ? max_ctas / 2 : 1;  // one CTA (4 warps) per SM
+        switch (a.nin) {
+            case 1: return launch_xor_tma_n<1>(a, ctas, s);
+            case 2: return launch_xor_tma_n<2>(a, ctas, s);
+            case 3: return launch_xor_tma_n<3>(a, ctas, s);
+            case 4: return launch_xor_tma_n<4>(a, ctas, s);
+            case 5: return launch_xor_tma_n<5>(a, ctas, s);
+            case 6: return launch_xor_tma_n<6>(a, ctas, s);
+            case 7: return launch_xor_tma_n<7>(a, ctas, s);
+            default: return launch_xor_tma_n<8>(a, ctas, s);
+        }
+    }
     switch (a.nin) {
         case 1: return launch_xor_n<1>(a, max_ctas, s);
         case 2: return launch_xor_n<2>(a, max_ctas, s);
