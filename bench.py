@@ -329,18 +329,19 @@ def main():
                                              "bytes_per_launch": per, "avg_launch_us": dur * 1e3,
                                              "launches": st["pack_launches"],
                                              "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy r+w)"}))
+    xor_name = "xor_kernel<m-1>" if os.environ.get("CKPT_XOR_IMPL") == "lsu" else "xor_tma_kernel<m-1>"
     if st["xor_launches"] and a.gather == "kernel":
         per = st["xor_bytes_in"] / st["xor_launches"]
         dur = st["xor_ms"] / st["xor_launches"]
         kern.append(("xor", st["xor_ms"], {"bound": "nvlink", "achieved": per / dur / 1e6, "peak": NVLINK_PEAK_GBS,
-                                           "unit": "GB/s", "kernel": "xor_kernel<m-1>", "bytes_per_launch": per,
+                                           "unit": "GB/s", "kernel": xor_name, "bytes_per_launch": per,
                                            "avg_launch_us": dur * 1e3, "launches": st["xor_launches"],
                                            "peak_source": "B200_PROFILING.md measured peer copy 770 GB/s/direction"}))
     elif st["xor_launches"]:  # CE gather: the XOR kernel reads local HBM (m-1 streams) and writes parity
         per = (st["xor_bytes_in"] + st["xor_bytes_out"]) / st["xor_launches"]
         dur = st["xor_ms"] / st["xor_launches"]
         kern.append(("xor", st["xor_ms"], {"bound": "hbm", "achieved": per / dur / 1e6, "peak": hbm_peak,
-                                           "unit": "GB/s", "kernel": "xor_kernel<m-1>", "bytes_per_launch": per,
+                                           "unit": "GB/s", "kernel": xor_name, "bytes_per_launch": per,
                                            "avg_launch_us": dur * 1e3, "launches": st["xor_launches"],
                                            "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy r+w)"}))
     kern.sort(key=lambda x: -x[1])
