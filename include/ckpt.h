@@ -281,7 +281,11 @@ int ckpt_rebuild(ckpt_ctx *ctx, int32_t lost_rank, void *stream);
  * (1) every lost member x whose ARC holder x-1 survived takes its completed image (and
  * parity row) from the holder's ARC copy; (2) a single remaining loss is rebuilt from
  * parity as in ckpt_rebuild; (3) the ARC copies held by lost members are re-created from
- * their neighbours' completed images.  Follow with ckpt_load on every member.
+ * their neighbours' completed images.  Follow with ckpt_load on every member.  With
+ * full-copy staging (and without CKPT_OPT_HOST_LOAD) step (1) goes device-first: an H2D
+ * of the holder's copy into the member's staging, so ckpt_load unpacks from HBM, while
+ * the member's own host image and the copy it holds are re-written by host threads in
+ * the background (ckpt_sync waits for them; every call that reads the host image does).
  * Errors: EUNRECOVERABLE (the losses exceed what the scheme restores), EINVAL, ENOSNAP,
  * ECUDA, EPEER. */
 int ckpt_recover(ckpt_ctx *ctx, uint32_t lost_mask, void *stream);

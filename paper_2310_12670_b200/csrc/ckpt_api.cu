@@ -202,6 +202,8 @@ extern "C" int ckpt_create(int device, const ckpt_options *o, ckpt_ctx **out) {
 
 extern "C" int ckpt_destroy(ckpt_ctx *c) {
     if (!c) return CKPT_OK;
+    for (auto &t : c->host_bg)  // background host copies of an ARC restore
+        if (t.joinable()) t.join();
     cudaSetDevice(c->device);
     cudaStream_t ss[5] = {c->sP, c->sX, c->sC, c->sW, c->sG};
     for (auto s : ss)

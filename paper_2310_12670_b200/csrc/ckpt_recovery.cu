@@ -89,6 +89,9 @@ int rb_finish(ckpt_ctx *c, uint32_t kl) {
 
 // Wait for a background host restore (see async_host_restore) and publish it.
 int host_sync(ckpt_ctx *c) {
+    for (auto &t : c->host_bg)
+        if (t.joinable()) t.join();
+    c->host_bg.clear();
     if (!c->host_pending) return CKPT_OK;
     int rc = set_dev(c);
     if (rc) return rc;
@@ -243,17 +246,48 @@ int recover_plan(const ckpt_ctx *c, uint32_t mask, int32_t *remaining) {
     return CKPT_OK;
 }
 
+// With full-copy staging and the device path allowed, the lost member's DEVICE image comes
+// first: H2D of the holder's copy into the staging and parity buffer (PCIe-bound -- the
+// floor for a member whose device memory is gone), after which ckpt_load unpacks from HBM;
+// its own host image is re-written from the holder's file by host threads in the
+// background (host_sync joins them before anything reads or overwrites the host image).
+static bool arc_device_first(const ckpt_ctx *c) {
+    return c->full_copy && !device_only(c) && !(c->opt.flags & CKPT_OPT_HOST_LOAD);
+}
+
 int recover_step1(ckpt_ctx *c, uint32_t mask, uint64_t version) {
     if (!(mask & (1u << c->me)) || !c->arc || (mask & (1u << holder_of(c, c->me)))) return CKPT_OK;
     int rc = ensure_holder_mapped(c);
     if (rc) return rc;
+    if ((rc = host_sync(c))) return rc;
     const int idx = rb_target(c);
     const uint64_t P = parity_bytes_of(c);
-    // only [0, L) carries data; the zero pad is written here, never copied (a peer's pad
-    // may still hold ckpt_forget poison while it is being cleaned)
-    parallel_memcpy(c->hdata[idx].p, c->shm_hold[idx].p + c->Lstar + P, c->L);
-    if (c->Lstar > c->L) memset(c->hdata[idx].p + c->L, 0, c->Lstar - c->L);
-    if (c->aec) parallel_memcpy(c->hpar[idx].p, c->shm_hold[idx].p + 2 * c->Lstar + P, P);
+    const uint8_t *src_d = c->shm_hold[idx].p + c->Lstar + P, *src_p = c->shm_hold[idx].p + 2 * c->Lstar + P;
+    auto host_copy = [c, idx, src_d, src_p, P] {
+        // only [0, L) carries data; the zero pad is written here, never copied (a peer's pad
+        // may still hold ckpt_forget poison while it is being cleaned)
+        parallel_memcpy(c->hdata[idx].p, src_d, c->L);
+        if (c->Lstar > c->L) memset(c->hdata[idx].p + c->L, 0, c->Lstar - c->L);
+        if (c->aec) parallel_memcpy(c->hpar[idx].p, src_p, P);
+    };
+    if (arc_device_first(c)) {
+        if ((rc = set_dev(c))) return rc;
+        // (full-copy staging holds [0, L) only: peers read the pad [L, L*) as zero, Q5)
+        CUDA_TRY(cudaMemcpyAsync(c->staging, src_d, c->L, cudaMemcpyHostToDevice, c->sC));
+        if (c->aec && P) CUDA_TRY(cudaMemcpyAsync(c->parity, src_p, P, cudaMemcpyHostToDevice, c->sC));
+        if ((rc = sync_stream_timeout(c, c->sC, "arc restore"))) return rc;
+        c->st.h2d_bytes += c->L + (c->aec ? P : 0);
+        c->st.ce_copies += (c->aec && P) ? 2 : 1;
+        c->staging_poisoned = false;
+        c->host_bg.emplace_back(host_copy);
+        c->pad_dirty[idx] = false;
+        c->completed = idx;
+        c->completed_id = version;
+        c->staging_id = version;
+        c->host_pending = true;  // meta is published by host_sync
+        return CKPT_OK;
+    }
+    host_copy();
     c->pad_dirty[idx] = false;
     c->completed = idx;
     c->completed_id = version;
@@ -269,10 +303,17 @@ int recover_step3(ckpt_ctx *c, uint32_t mask) {
     if (idx < 0) return fail(CKPT_ESTATE, "recover: member %u has no completed image after restore", c->me);
     const uint64_t P = parity_bytes_of(c);
     const uint64_t Ln = c->peer_L[(c->me + 1) % c->m];
-    parallel_memcpy(c->harc[idx], c->shm_next[idx].p, Ln);  // member me+1's data ...
-    if (c->Lstar > Ln) memset(c->harc[idx] + Ln, 0, c->Lstar - Ln);  // ... and a clean pad
-    if (c->aec) parallel_memcpy(c->harcp[idx], c->shm_next[idx].p + c->Lstar, P);
+    auto host_copy = [c, idx, P, Ln] {
+        parallel_memcpy(c->harc[idx], c->shm_next[idx].p, Ln);  // member me+1's data ...
+        if (c->Lstar > Ln) memset(c->harc[idx] + Ln, 0, c->Lstar - Ln);  // ... and a clean pad
+        if (c->aec) parallel_memcpy(c->harcp[idx], c->shm_next[idx].p + c->Lstar, P);
+    };
     c->arc_dirty[idx] = false;
+    if (arc_device_first(c)) {  // host-only work: in the background as well
+        c->host_bg.emplace_back(host_copy);
+        return CKPT_OK;
+    }
+    host_copy();
     return CKPT_OK;
 }
 
