@@ -828,7 +828,10 @@ cudaError_t launch_xor(const XorArgs &a, int max_ctas, cudaStream_t s) {
         aligned = aligned && ((uintptr_t)a.in[k].base & 15) == 0 && (a.in[k].stride & 15) == 0 &&
                   (a.in[k].off & 15) == 0 && (a.in[k].valid & 15) == 0;
     if (impl == 1 && aligned) {
-        const int ctas = max_ctas / 2 > 0 ? max_ctas / 2 : 1;  // one CTA (4 warps) per SM
+        // one CTA (4 warps, ~190 KiB of loads in flight) per SM; 32 SMs already pull what
+        // NVLink delivers (m=2: 673 vs 678 GB/s on 148 SMs; m=4: 611 vs 607), so the
+        // default leaves the other SMs to the training kernels (CKPT_XOR_CTAS overrides)
+        const int ctas = cap > 0 ? std::max(1, max_ctas / 2) : std::max(1, std::min(32, max_ctas / 2));
         switch (a.nin) {
             case 1: return launch_xor_tma_n<1>(a, ctas, s);
             case 2: return launch_xor_tma_n<2>(a, ctas, s);
