@@ -172,3 +172,25 @@ def test_aor_options_and_protocol_guard(C):
     with pytest.raises(C.CkptError) as e:
         C.aor_recover(0, 0b0110, 1, 4, barrier=lambda: None)
     assert e.value.code == C.CKPT_EUNRECOVERABLE
+
+
+def test_c_program_uses_the_abi(C, tmp_path):
+    """examples/plan_from_c.c: the library from plain C (gcc, include/*.h, -lreft_ckpt), its
+    host-only results checked against the oracle and the Q22 closed form."""
+    import struct
+    import subprocess
+    libdir = os.path.dirname(C.LIB_PATH)
+    exe = str(tmp_path / "plan_from_c")
+    subprocess.check_call(["gcc", "-std=c99", "-Wall", "-Werror", "-I", os.path.join(ROOT, "include"),
+                           os.path.join(ROOT, "examples", "plan_from_c.c"), "-L", libdir, "-lreft_ckpt",
+                           f"-Wl,-rpath,{libdir}", "-o", exe])
+    out = dict(line.split(" ", 1) for line in subprocess.check_output([exe], text=True).splitlines())
+    off, L = oracle.layout([1000, 4096, 1, 70000, 255], 256)
+    assert out["layout"] == f"rc=0 L={L} off={','.join(map(str, off))}"
+    Ls, ue = oracle.common_length([L, 1280, 99840], 4096)
+    assert out["common"] == f"rc=0 Lstar={Ls} unit={ue}"
+    assert out["has"] == "rc=0 t_ss=10.000 t_bubble=4.000 bubble=40 compute=60"
+    want = [struct.unpack("<I", struct.pack("<f", x))[0] for x in (1.0 - 0.125, -3.5 + 0.0625, 1024.0 - 2.0)]
+    assert out["aor"] == "rc=0 w=" + ",".join(f"{x:08x}" for x in want)
+    assert out["bad"].startswith("rc=-1 (invalid argument)")
+    assert "sm_100a" in out["version"]
