@@ -591,3 +591,21 @@ def test_has_window_gates_the_d2h(torch, C):
         assert_bytes_equal(C.ckpt_host_view(ctx, 0, copy=True)[0], want, "image after the window opened")
     finally:
         C.ckpt_destroy(ctx)
+
+
+@pytest.mark.parametrize("m,lost", [(2, 0), (4, 1), (5, 4)])
+def test_c_program_drill(torch, C, tmp_path, m, lost):
+    """examples/drill_from_c.c: snapshot + parity, loss, rebuild and load through the C ABI
+    alone (gcc, include/ckpt.h, -lreft_ckpt -lcudart), tensors checked byte for byte."""
+    import os
+    import subprocess
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    libdir = os.path.dirname(C.LIB_PATH)
+    exe = str(tmp_path / "drill")
+    subprocess.check_call(["gcc", "-std=c99", "-Wall", "-Werror", "-I", os.path.join(root, "include"),
+                           "-I", "/usr/local/cuda/include", os.path.join(root, "examples", "drill_from_c.c"),
+                           "-L", libdir, "-lreft_ckpt", "-L", "/usr/local/cuda/lib64", "-lcudart",
+                           f"-Wl,-rpath,{libdir}:/usr/local/cuda/lib64", "-o", exe])
+    r = subprocess.run([exe, str(m), str(lost)], capture_output=True, text=True, timeout=120)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert r.stdout.strip() == f"ok m={m} lost={lost}"
