@@ -400,7 +400,10 @@ int ckpt_aor_create(int device, const ckpt_aor_options *o, const ckpt_aor_shard 
     // The replica object this member holds: re-attach (same key: a restarted process) or create.
     const std::string name = aor_name(opt.key, a->me);
     const uint64_t obytes = kAorHdr + a->n_rep * 4;
-    int rc = shm_attach(a->own, name, obytes, true);
+    // pinned only when this member is its own holder (m = 1: seed and restore copy it over
+    // PCIe); otherwise only host threads touch it
+    const bool own_reg = a->holder == a->me;
+    int rc = shm_attach(a->own, name, obytes, own_reg);
     if (rc == CKPT_OK) {
         AorHdr *h = (AorHdr *)a->own.p;
         if (h->magic != kAorMagic || h->version != kAorVersion || h->key != opt.key || h->owner != a->owner ||
@@ -409,7 +412,7 @@ int ckpt_aor_create(int device, const ckpt_aor_options *o, const ckpt_aor_shard 
             return fail(CKPT_EMISMATCH, "aor_create: existing object %s describes another geometry", name.c_str());
         }
     } else if (rc == CKPT_ENOSNAP) {
-        if ((rc = shm_create(a->own, name, obytes)) != CKPT_OK) return rc;
+        if ((rc = shm_create(a->own, name, obytes, own_reg)) != CKPT_OK) return rc;
         a->own.kind = kShmPeer;  // unlinked explicitly by destroy (unless persistent)
         AorHdr *h = (AorHdr *)a->own.p;
         h->magic = kAorMagic;

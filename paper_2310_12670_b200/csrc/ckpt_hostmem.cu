@@ -129,7 +129,7 @@ std::string shm_name(uint64_t nonce, uint32_t member, int buf) {
     return s;
 }
 
-int shm_create(HostBuf &b, const std::string &name, uint64_t bytes) {
+int shm_create(HostBuf &b, const std::string &name, uint64_t bytes, bool reg) {
     b = HostBuf{};
     const uint64_t len = align_up(std::max<uint64_t>(bytes, 1), 2ull << 20);
     int fd = shm_open(name.c_str(), O_CREAT | O_EXCL | O_RDWR, 0600);
@@ -149,7 +149,7 @@ int shm_create(HostBuf &b, const std::string &name, uint64_t bytes) {
     madvise(p, len, MADV_HUGEPAGE);
 #endif
     prefault((uint8_t *)p, len);  // allocates the tmpfs pages (zero-filled)
-    if (cudaHostRegister(p, len, cudaHostRegisterPortable) != cudaSuccess) {
+    if (reg && cudaHostRegister(p, len, cudaHostRegisterPortable) != cudaSuccess) {
         cudaGetLastError();
         munmap(p, len);
         shm_unlink(name.c_str());
@@ -158,7 +158,7 @@ int shm_create(HostBuf &b, const std::string &name, uint64_t bytes) {
     b.p = (uint8_t *)p;
     b.bytes = len;
     b.kind = kShmOwn;
-    b.registered = true;
+    b.registered = reg;
     b.name = name;
     return CKPT_OK;
 }

@@ -311,7 +311,7 @@ void prefault(uint8_t *p, uint64_t len);
 void parallel_memcpy(uint8_t *dst, const uint8_t *src, uint64_t n);
 int host_alloc(HostBuf &b, uint64_t bytes);
 std::string shm_name(uint64_t nonce, uint32_t member, int buf);
-int shm_create(HostBuf &b, const std::string &name, uint64_t bytes);
+int shm_create(HostBuf &b, const std::string &name, uint64_t bytes, bool reg = true);
 int shm_map(HostBuf &b, const std::string &name, uint64_t bytes, bool reg);
 int shm_attach(HostBuf &b, const std::string &name, uint64_t bytes, bool reg);
 std::string meta_name(uint64_t key, uint32_t member);
