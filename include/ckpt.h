@@ -336,13 +336,27 @@ int ckpt_arena_unlink(uint64_t key, uint32_t m, uint32_t nbuf);
  * Placement of the snapshot's host traffic relative to training.  With copy engines the
  * D2H can overlap anything; what it still disturbs is HBM-bound training work (measured:
  * a concurrent 57 GB/s D2H slows an HBM-bound kernel by 10-35%, tools/ce_interference.py).
- * ckpt_window(ctx, open, stream) enqueues on the TRAINING stream a write of the
- * context's window flag (1 = open, 0 = closed; open at creation).  With CKPT_OPT_WINDOWED
- * every bucket's D2H first waits (on the copy engine's stream, zero SMs) for an open
- * window, so the caller opens it around bubbles and compute-bound phases (layers 1 and 2)
- * and closes it around HBM-bound phases.  A snapshot whose window is never reopened does
- * not complete (ckpt_wait times out). */
+ * ckpt_window(ctx, open, stream) enqueues on the TRAINING stream a write of the context's
+ * window word: a mask of CKPT_WINDOW_BUBBLE (pipeline bubbles, Alg 1 lines 9-12) and
+ * CKPT_WINDOW_COMPUTE (compute-bound phases, layers 1-2, P.419-425); 0 closes both (both
+ * are open at creation).  With CKPT_OPT_WINDOWED every bucket's D2H (data and parity)
+ * first waits, on the copy engine's stream (zero SMs), until its window is open.  Which
+ * buckets wait for which window is Alg 1's SplitParameter, applied by ckpt_has_apply:
+ * the first bubble_bytes of the image (whole buckets) go out only in bubbles, the rest
+ * alongside computation or in a bubble (reading Q26); by default every bucket is a bubble
+ * bucket.  Buckets leave in image order.  A snapshot whose windows are
+ * never reopened does not complete (ckpt_wait times out). */
+#define CKPT_WINDOW_BUBBLE  0x1u
+#define CKPT_WINDOW_COMPUTE 0x2u
 int ckpt_window(ckpt_ctx *ctx, int open, void *stream);
+
+/* Alg 1 SplitParameter into the scheduler (lines 10-12): image bytes [0, bubble_bytes),
+ * rounded up to whole buckets at each snapshot, are snapshotted in CKPT_WINDOW_BUBBLE
+ * windows, the rest in CKPT_WINDOW_COMPUTE (or bubble) windows (use ckpt_has_plan's
+ * bubble_bytes).
+ * UINT64_MAX (the default) = all in bubbles.  Takes effect at the next snapshot.
+ * Errors: EINVAL. */
+int ckpt_has_apply(ckpt_ctx *ctx, uint64_t bubble_bytes);
 
 /* Alg 1's estimators, host-only.  EstimateSnapshotTime = bytes / B_io; EstimateBubbleTime
  * = (0.8 p + 2|P| - p - 2) * C_FB,BP (1F1B, stage p of |P|, clamped at 0); SplitParameter:

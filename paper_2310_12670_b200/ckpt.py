@@ -143,6 +143,7 @@ def lib():
             "ckpt_recover": (ctypes.c_int, [_vp, _u32, _vp]),
             "ckpt_sync": (ctypes.c_int, [_vp]),
             "ckpt_window": (ctypes.c_int, [_vp, ctypes.c_int, _vp]),
+            "ckpt_has_apply": (ctypes.c_int, [_vp, _u64]),
             "ckpt_has_plan": (ctypes.c_int, [_u32, _u32, ctypes.c_double, _u64, ctypes.c_double,
                                              ctypes.POINTER(ckpt_has_plan_t)]),
             "ckpt_forget": (ctypes.c_int, [_vp, ctypes.c_uint8]),
@@ -316,9 +317,20 @@ def ckpt_recover(ctx: int, lost_mask: int, stream=None) -> None:
     _check(lib().ckpt_recover(ctx, lost_mask, _stream_handle(stream)), "ckpt_recover")
 
 
-def ckpt_window(ctx: int, open_: bool, stream=None) -> None:
-    """HAS: open/close the snapshot window at the current position of the training stream."""
-    _check(lib().ckpt_window(ctx, 1 if open_ else 0, _stream_handle(stream)), "ckpt_window")
+CKPT_WINDOW_BUBBLE, CKPT_WINDOW_COMPUTE = 0x1, 0x2
+
+
+def ckpt_window(ctx: int, open_, stream=None) -> None:
+    """Write the HAS window mask on `stream` (True = both windows, False = closed)."""
+    if open_ is True:
+        open_ = CKPT_WINDOW_BUBBLE | CKPT_WINDOW_COMPUTE
+    elif open_ is False:
+        open_ = 0
+    _check(lib().ckpt_window(ctx, int(open_), _stream_handle(stream)), "ckpt_window")
+
+
+def ckpt_has_apply(ctx: int, bubble_bytes: int) -> None:
+    _check(lib().ckpt_has_apply(ctx, bubble_bytes), "ckpt_has_apply")
 
 
 def ckpt_has_plan(stage: int, num_stages: int, c_fb_bp_s: float, snapshot_bytes: int, b_io: float) -> dict:

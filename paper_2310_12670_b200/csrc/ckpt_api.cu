@@ -189,8 +189,8 @@ extern "C" int ckpt_create(int device, const ckpt_options *o, ckpt_ctx **out) {
     if (e == cudaSuccess) e = cudaEventCreate(&c->ev_t1);
     if (e == cudaSuccess) e = cudaMalloc(&c->window, 256);
     if (e == cudaSuccess) {
-        const uint32_t one = 1;  // windows start open
-        e = cudaMemcpy(c->window, &one, sizeof one, cudaMemcpyHostToDevice);
+        const uint32_t all = CKPT_WINDOW_BUBBLE | CKPT_WINDOW_COMPUTE;  // windows start open
+        e = cudaMemcpy(c->window, &all, sizeof all, cudaMemcpyHostToDevice);
     }
     if (e != cudaSuccess) {
         ckpt_destroy(c);
@@ -712,9 +712,17 @@ extern "C" int ckpt_window(ckpt_ctx *c, int open, void *stream) {
     if (load_memops()) return fail(CKPT_ECUDA, "window: stream memory operations unavailable");
     int rc = set_dev(c);
     if (rc) return rc;
-    CUresult r = p_write32((CUstream)stream, (CUdeviceptr)(uintptr_t)c->window, open ? 1u : 0u,
+    if (open < 0 || (open & ~(int)(CKPT_WINDOW_BUBBLE | CKPT_WINDOW_COMPUTE)))
+        return fail(CKPT_EINVAL, "window: open must be a mask of CKPT_WINDOW_BUBBLE | CKPT_WINDOW_COMPUTE");
+    CUresult r = p_write32((CUstream)stream, (CUdeviceptr)(uintptr_t)c->window, (uint32_t)open,
                            CU_STREAM_WRITE_VALUE_DEFAULT);
     if (r != CUDA_SUCCESS) return fail(CKPT_ECUDA, "cuStreamWriteValue32(window) failed (%d)", (int)r);
+    return CKPT_OK;
+}
+
+extern "C" int ckpt_has_apply(ckpt_ctx *c, uint64_t bubble_bytes) {
+    if (!c) return fail(CKPT_EINVAL, "has_apply: null");
+    c->has_bubble_bytes = bubble_bytes;
     return CKPT_OK;
 }
 

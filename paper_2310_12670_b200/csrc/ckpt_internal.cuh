@@ -150,7 +150,8 @@ struct ckpt_ctx {
     uint64_t staging_bytes = 0;
     uint32_t *flags = nullptr;  // local flag page (device), written by peers
     uint32_t *counters = nullptr;  // per-bucket CTA completion counters (single-launch pack)
-    uint32_t *window = nullptr;    // HAS window flag (device, bit 0 = open), written by memops
+    uint32_t *window = nullptr;    // HAS window word (device, CKPT_WINDOW_* mask), written by memops
+    uint64_t has_bubble_bytes = UINT64_MAX;  // Alg 1 split: image bytes snapshotted in bubbles
 
     // group
     bool grouped = false;  // ckpt_protect succeeded (m >= 2) or m == 1 arena set up
@@ -264,6 +265,14 @@ static inline uint8_t *slot_ptr(const ckpt_ctx *c, uint8_t *base, uint64_t k) {
 static inline uint8_t *parity_slot_ptr(const ckpt_ctx *c, uint64_t k) {
     return c->full_copy ? c->parity + bucket_begin(c, k) / (c->m - 1)
                         : c->parity + (uint64_t)(k % c->n_slots) * c->parity_slot_bytes;
+}
+
+// Alg 1 placement of bucket k (ckpt_has_apply): the buckets that start below the split
+// go out only in bubbles; the others alongside computation -- or in a bubble, which is
+// never worse (reading Q26).  The wait passes when (window & mask) != 0.
+static inline uint32_t window_of(const ckpt_ctx *c, uint64_t k) {
+    return bucket_begin(c, k) < c->has_bubble_bytes ? CKPT_WINDOW_BUBBLE
+                                                    : (CKPT_WINDOW_BUBBLE | CKPT_WINDOW_COMPUTE);
 }
 
 static inline uint32_t bucket_seq(const ckpt_ctx *c, uint64_t k) { return c->op_seq_base + (uint32_t)k + 1; }

@@ -454,8 +454,9 @@ int stage_copy(ckpt_ctx *c, uint64_t k, bool with_parity) {
         CUDA_TRY(cudaEventRecord(c->ev_d2h_data[s], c->sC));
         return with_parity ? stage_copy_parity(c, k) : CKPT_OK;
     }
-    if (v && (c->opt.flags & CKPT_OPT_WINDOWED)) {  // HAS: only while the window is open
-        CUresult r = p_wait32((CUstream)c->sC, (CUdeviceptr)(uintptr_t)c->window, 1u, CU_STREAM_WAIT_VALUE_AND);
+    if (v && (c->opt.flags & CKPT_OPT_WINDOWED)) {  // HAS: only while its window is open
+        CUresult r = p_wait32((CUstream)c->sC, (CUdeviceptr)(uintptr_t)c->window, window_of(c, k),
+                              CU_STREAM_WAIT_VALUE_AND);
         if (r != CUDA_SUCCESS) return fail(CKPT_ECUDA, "cuStreamWaitValue32(window) failed (%d)", (int)r);
     }
     if (v) {
@@ -479,7 +480,8 @@ int stage_copy_parity(ckpt_ctx *c, uint64_t k) {
     const uint64_t pb = (be - bb) / (c->m - 1);
     CUDA_TRY(cudaStreamWaitEvent(c->sC, c->ev_xored[s], 0));
     if (!device_only(c) && (c->opt.flags & CKPT_OPT_WINDOWED)) {
-        CUresult r = p_wait32((CUstream)c->sC, (CUdeviceptr)(uintptr_t)c->window, 1u, CU_STREAM_WAIT_VALUE_AND);
+        CUresult r = p_wait32((CUstream)c->sC, (CUdeviceptr)(uintptr_t)c->window, window_of(c, k),
+                              CU_STREAM_WAIT_VALUE_AND);
         if (r != CUDA_SUCCESS) return fail(CKPT_ECUDA, "cuStreamWaitValue32(window) failed (%d)", (int)r);
     }
     if (!device_only(c)) {

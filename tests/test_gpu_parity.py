@@ -593,6 +593,44 @@ def test_has_window_gates_the_d2h(torch, C):
         C.ckpt_destroy(ctx)
 
 
+def test_has_split_places_buckets_in_their_windows(torch, C):
+    """Alg 1 SplitParameter in the scheduler (ckpt_has_apply): the first bubble_bytes of the
+    image go out only in CKPT_WINDOW_BUBBLE windows (they lead, so a compute window moves
+    nothing); the rest in CKPT_WINDOW_COMPUTE or bubble windows (Q26); committed images
+    match the oracle."""
+    import time
+    st = tiny(0, n=9)
+    specs, ts = st
+    B = 1 << 16
+    ctx = make_ctx(C, st, n_slots=0, bucket_bytes=B, flags=C.CKPT_OPT_WINDOWED)
+    s = torch.cuda.Stream()
+    try:
+        C.ckpt_protect(ctx, 1, 0)
+        g = C.ckpt_geometry(ctx)
+        assert g["L"] > 2 * B
+        want, _, _ = oracle_image(specs, 0, g["L_star"])
+        C.ckpt_has_apply(ctx, B + 1)                     # rounds up to two whole buckets
+        C.ckpt_window(ctx, C.CKPT_WINDOW_COMPUTE, s)     # a compute phase: the bubble part waits
+        sid = C.ckpt_snapshot(ctx, 0, s)
+        time.sleep(0.3)
+        assert not C.ckpt_host_view(ctx, 1, copy=True)[0].any(), "bubble buckets left outside a bubble"
+        C.ckpt_window(ctx, C.CKPT_WINDOW_BUBBLE, s)      # a bubble: everything may go
+        C.ckpt_wait(ctx, sid)
+        assert_bytes_equal(C.ckpt_host_view(ctx, 0, copy=True)[0], want, "image after a bubble")
+        C.ckpt_has_apply(ctx, 0)                         # all alongside computation
+        C.ckpt_window(ctx, 0, s)                         # an HBM-bound phase: closed
+        sid = C.ckpt_snapshot(ctx, 0, s)
+        time.sleep(0.3)
+        assert not C.ckpt_host_view(ctx, 1, copy=True)[0].any(), "D2H while every window was closed"
+        C.ckpt_window(ctx, C.CKPT_WINDOW_COMPUTE, s)
+        C.ckpt_wait(ctx, sid)
+        assert_bytes_equal(C.ckpt_host_view(ctx, 0, copy=True)[0], want, "image after a compute window")
+        with pytest.raises(C.CkptError):
+            C.ckpt_window(ctx, 4, s)
+    finally:
+        C.ckpt_destroy(ctx)
+
+
 @pytest.mark.parametrize("m,lost", [(2, 0), (4, 1), (5, 4)])
 def test_c_program_drill(torch, C, tmp_path, m, lost):
     """examples/drill_from_c.c: snapshot + parity, loss, rebuild and load through the C ABI
