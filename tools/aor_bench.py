@@ -131,6 +131,10 @@ def run_config(a, C, np, torch, oracle, bar, amax, amin, key, chunk_mib, threads
            "host_update_gbs_per_rank": round(upd_gbs, 2),
            "host_roofline_gbs_per_rank": round(amin(roof), 2), "host_roofline_threads": default_threads,
            "host_update_frac": round(upd_gbs / amin(roof), 3) if roof else None,
+           # the whole step against host DRAM: D2H write + Eq 4 (esz + bpe bytes per element)
+           # at this rank's share of the all-ranks routine bandwidth
+           "replica_roofline_ms": round((esz + bpe) * n_rep / (amin(roof) * 1e9) * 1e3, 2) if roof else None,
+           "replica_roofline_frac": round((esz + bpe) * n_rep / (amin(roof) * 1e9) * 1e3 / repl, 3) if roof else None,
            "stall_s_rank0": round(st["stall_s"], 3), "create_s_rank0": round(create_s, 2),
            "bit_exact_sampled": okall, "samples_per_rank": int(idx.size), "gemm_corun": corun}
     if rank == 0:
