@@ -647,3 +647,17 @@ def test_c_program_drill(torch, C, tmp_path, m, lost):
     r = subprocess.run([exe, str(m), str(lost)], capture_output=True, text=True, timeout=120)
     assert r.returncode == 0, r.stdout + r.stderr
     assert r.stdout.strip() == f"ok m={m} lost={lost}"
+
+
+@pytest.mark.parametrize("impl", ["lsu", "tma"])
+def test_smoke_with_each_xor_kernel(torch, C, impl):
+    """Both XOR implementations (CKPT_XOR_IMPL is read once per process, hence a subprocess):
+    __graft_entry__.smoke() -- m=4 snapshot + parity, rebuild, load -- bit-exact vs the oracle."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, CKPT_XOR_IMPL=impl)
+    r = subprocess.run([sys.executable, os.path.join(root, "__graft_entry__.py"), "smoke"], cwd=root, env=env,
+                       capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0 and "smoke ok" in r.stdout, r.stdout[-2000:] + r.stderr[-2000:]
