@@ -153,10 +153,13 @@ extern "C" int ckpt_rebuild(ckpt_ctx *c, int32_t lost, void *stream) {
 int rebuild_aec(ckpt_ctx *c, int32_t lost, void *stream) {
     NvtxRange nvtx_("ckpt_rebuild");
     if (!c) return fail(CKPT_EINVAL, "rebuild: null");
-    if (host_sync(c)) return CKPT_ECUDA;
     if (!c->registered || !c->grouped) return fail(CKPT_ESTATE, "rebuild: not protected");
     if (c->m < 2) return fail(CKPT_EUNRECOVERABLE, "rebuild: a group of one has no redundancy (P.460)");
     if (lost < 0 || (uint32_t)lost >= c->m) return fail(CKPT_EINVAL, "rebuild: lost rank %d out of range", lost);
+    // a survivor that serves the rebuild from its device image touches no host buffer: a
+    // background host restore (e.g. of an ARC restore just before, in ckpt_recover) may
+    // keep running; the lost member and host-path survivors wait for it
+    if ((c->me == (uint32_t)lost || !device_image_valid(c)) && host_sync(c)) return CKPT_ECUDA;
     if (!c->aec) return fail(CKPT_EUNRECOVERABLE, "rebuild: the scheme has no parity");
     int rc = check_sticky(c);
     if (rc) return rc;
