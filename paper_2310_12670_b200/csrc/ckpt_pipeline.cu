@@ -740,7 +740,23 @@ extern "C" int ckpt_load(ckpt_ctx *c, void *stream) {
     const bool from_dev = device_image_valid(c);
     CUDA_TRY(cudaStreamWaitEvent(from_dev ? c->sP : c->sC, c->ev_capture, 0));
     const uint8_t *img = from_dev ? nullptr : c->hdata[c->completed].p;
-    for (uint64_t k = 0; k < c->op_NB; ++k) {
+    if (from_dev && c->full_copy && !(c->opt.flags & CKPT_OPT_CE_PACK)) {
+        // the whole completed image is in HBM: ONE unpack launch over [0, L) (no per-bucket
+        // launches or tails; nothing waits on the copy stream)
+        PackArgs a;
+        a.chunks = c->d_chunks;
+        a.tile_first = c->d_tile_first;
+        a.bucket_begin = 0;
+        a.bucket_end = c->L;
+        a.slot = c->staging;
+        a.unpack = 1;
+        TimedLaunch *t;
+        if ((rc = timed_begin(c, c->sP, 2, &t))) return rc;
+        CUDA_TRY(launch_pack(a, c->max_ctas, c->sP, false));
+        if ((rc = timed_end(t, c->sP))) return rc;
+        c->st.unpack_launches++;
+    }
+    for (uint64_t k = 0; k < c->op_NB && !(from_dev && c->full_copy && !(c->opt.flags & CKPT_OPT_CE_PACK)); ++k) {
         const uint32_t s = slot_of(c, k);
         const uint64_t bb = bucket_begin(c, k);
         const uint64_t v = valid_in_bucket(c->L, bb, bucket_end(c, k));
