@@ -243,6 +243,7 @@ __device__ __forceinline__ void st_release_sys(uint32_t *p, uint32_t v) {
 // Publish bucket k: count this CTA's `cnt` finished groups; the CTA completing the
 // bucket stores its flag (release, system scope) locally and into every peer's page.
 __device__ __noinline__ void publish_bucket(const PackAllArgs &g, uint32_t k, uint32_t cnt, uint32_t need) {
+    if (g.unpack) return;
     // this CTA's stores (ordered by the preceding barrier) before the count: acq_rel at
     // gpu scope is enough here (__threadfence is the heavier fence.sc)
     asm volatile("fence.acq_rel.gpu;" ::: "memory");
@@ -261,7 +262,7 @@ __global__ void __launch_bounds__(kPackThreads, 2) pack_all_kernel(const __grid_
     a.bucket_begin = 0;
     a.bucket_end = g.L;
     a.slot = g.image;
-    a.unpack = 0;
+    a.unpack = g.unpack;
     const uint32_t ntiles = (uint32_t)((g.L + kTile - 1) / kTile);
     const uint32_t ngroups = (uint32_t)((g.L + kGroup - 1) / kGroup);
     const uint32_t gpb = (uint32_t)(g.bucket / kGroup);  // groups per bucket
@@ -485,7 +486,7 @@ __global__ void __launch_bounds__(32 * W) pack_all_tma_kernel(const __grid_const
     a.bucket_begin = 0;
     a.bucket_end = g.L;
     a.slot = g.image;
-    a.unpack = 0;
+    a.unpack = g.unpack;
     const uint32_t ntiles = (uint32_t)((g.L + kTile - 1) / kTile);
     const uint32_t ngroups = (uint32_t)((g.L + kGroup - 1) / kGroup);
     const uint32_t gpb = (uint32_t)(g.bucket / kGroup);

@@ -81,6 +81,7 @@ struct PackAllArgs {
     int npeers;
     uint32_t seq_base;
     uint32_t maxb;
+    int unpack;            // 1: the load direction (image -> tensors), nothing is published
 };
 
 // Cross-rank signal by a one-warp kernel: st.release.sys of `value` to every address

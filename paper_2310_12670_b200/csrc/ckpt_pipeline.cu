@@ -743,16 +743,17 @@ extern "C" int ckpt_load(ckpt_ctx *c, void *stream) {
     if (from_dev && c->full_copy && !(c->opt.flags & CKPT_OPT_CE_PACK)) {
         // the whole completed image is in HBM: ONE unpack launch over [0, L) (no per-bucket
         // launches or tails; nothing waits on the copy stream)
-        PackArgs a;
+        PackAllArgs a;
+        memset(&a, 0, sizeof a);
         a.chunks = c->d_chunks;
         a.tile_first = c->d_tile_first;
-        a.bucket_begin = 0;
-        a.bucket_end = c->L;
-        a.slot = c->staging;
+        a.L = c->L;
+        a.image = c->staging;
+        a.bucket = align_up(std::max<uint64_t>(c->L, 1), kGroup);  // one "bucket": nothing to publish
         a.unpack = 1;
         TimedLaunch *t;
         if ((rc = timed_begin(c, c->sP, 2, &t))) return rc;
-        CUDA_TRY(launch_pack(a, c->max_ctas, c->sP, false));
+        CUDA_TRY(launch_pack_all(a, c->max_ctas, c->sP, !(c->opt.flags & CKPT_OPT_LSU_PACK)));
         if ((rc = timed_end(t, c->sP))) return rc;
         c->st.unpack_launches++;
     }
