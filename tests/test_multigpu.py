@@ -553,3 +553,83 @@ def _run_fn(fn, world, timeout=300):
 
 def test_aor_zero1_members_all_gpus():
     _run_fn(_aor_worker, min(_world(), 8))
+
+
+# ---------------------------------------------------------------- f3: group restart -------
+def _persist_worker(phase, key, drop, rank, world, port, q):
+    """phase 'write': commit v1 and v2 (tensors mutated between), start v3, every process
+    dies.  phase 'read': a NEW process per GPU re-attaches the persistent arena through the
+    IPC handshake (the group's committed version = v2), member `drop` first lost its host
+    memory (its shm files are gone) and is recovered from parity, then every member loads."""
+    try:
+        os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank), WORLD_SIZE=str(world))
+        import torch
+        import torch.distributed as dist
+
+        import synth
+        from paper_2310_12670_b200 import ckpt as C
+        from synth.gpu import alloc_state, descriptors, fill_state
+
+        torch.cuda.set_device(rank)
+        dev = torch.device("cuda", rank)
+        dist.init_process_group("nccl", device_id=dev)
+        specs = synth.config_tensors("tiny_7", rank)
+        ts = alloc_state(specs, dev, misalign=1)
+        if phase == "read" and drop == rank:
+            for b in range(2):
+                try:
+                    os.unlink(f"/dev/shm/reft-{key:016x}-{rank}-{b}")
+                except FileNotFoundError:
+                    pass
+        dist.barrier()
+        o = C.ckpt_options_default(n_slots=0, bucket_bytes=1 << 16, stripe_unit=4096,
+                                   flags=C.CKPT_OPT_SHM_ARENA, arena_key=key)
+        ctx = C.ckpt_create(rank, o)
+        C.ckpt_register(ctx, descriptors(ts, specs), {"local_rank": rank})
+        C.protect_ipc(ctx)
+        ok = []
+        if phase == "write":
+            fill_state(ts, rank)
+            for seed in (None, 31):
+                if seed is not None:
+                    fill_state(ts, rank, seed=seed, xor_mode=1)
+                sid = C.ckpt_snapshot(ctx)
+                C.ckpt_wait(ctx, sid)
+            fill_state(ts, rank, seed=32, xor_mode=1)
+            dist.barrier()
+            C.ckpt_snapshot(ctx)                  # v3 in flight when every process dies
+            q.put((rank, [True], None))
+            q.close()
+            q.join_thread()
+            os._exit(0)
+        for t in ts:
+            t.view(torch.uint8).fill_(0x77)       # fresh process: garbage in the tensors
+        if drop >= 0:
+            C.ckpt_recover(ctx, 1 << drop)
+        C.ckpt_load(ctx)
+        torch.cuda.synchronize()
+        for t, x in enumerate(ts):
+            want = synth.fill(synth.SEED, rank, t, specs[t].nbytes) ^ synth.fill(31, rank, t, specs[t].nbytes)
+            ok.append(bool(np.array_equal(x.contiguous().view(torch.uint8).cpu().numpy(), want)))
+        C.ckpt_destroy(ctx)
+        dist.barrier()
+        dist.destroy_process_group()
+        q.put((rank, ok, None))
+    except Exception:
+        q.put((rank, None, traceback.format_exc()))
+
+
+@pytest.mark.parametrize("drop", [-1, 1])
+def test_group_restart_reattaches_over_ipc(drop):
+    """SURVEY 8(f) f3 across GPUs: the whole group dies (as a TorchElastic restart would
+    have it) after committing v2 and while v3 is in flight; new processes re-attach,
+    agree on v2 through the handshake, recover a member without host memory, and load v2."""
+    import functools
+    world = min(_world(), 4)
+    key = int.from_bytes(os.urandom(8), "little") | 1
+    from paper_2310_12670_b200 import ckpt as C
+    try:
+        _run_fn(functools.partial(_persist_worker, "write", key, drop), world)
+        _run_fn(functools.partial(_persist_worker, "read", key, drop), world)
+    finally:
+        C.ckpt_arena_unlink(key, world, 2)
