@@ -194,6 +194,7 @@ struct ckpt_ctx {
     uint64_t staging_id = 0;  // id of the image the device staging + parity hold (0: none)
     bool staging_poisoned = false;  // ckpt_forget wrote over the staging's zero gaps
     bool host_pending = false;      // a rebuilt image is still being copied to host (ev_done)
+    bool done_enqueued = false;     // the snapshot's completion waits already sit on sW
     std::vector<std::thread> host_bg;  // background host copies of an ARC restore (host_sync joins)
 
     // streams / events

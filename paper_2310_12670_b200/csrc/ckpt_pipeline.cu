@@ -505,7 +505,17 @@ int stage_finish(ckpt_ctx *c) {
     if (c->m >= 2 && c->aec) CUDA_TRY(cudaStreamWaitEvent(c->sC, c->ev_xored[slot_of(c, c->op_NB ? c->op_NB - 1 : 0)], 0));
     CUDA_TRY(cudaEventRecord(c->ev_done, c->sC));
     if (c->opt.flags & CKPT_OPT_TIMING) CUDA_TRY(cudaEventRecord(c->ev_t1, c->sC));
-    if (c->m >= 2) return sig_signal(c, c->sC, kDone, c->op_seq_base + (uint32_t)c->op_NB + 1, 0);
+    const uint32_t done_seq = c->op_seq_base + (uint32_t)c->op_NB + 1;
+    int rc;
+    if (c->m >= 2 && (rc = sig_signal(c, c->sC, kDone, done_seq, 0))) return rc;
+    static const bool legacy = getenv("CKPT_WAIT_LEGACY") != nullptr;  // A/B knob
+    if (!legacy && (c->m < 2 || c->transport == CKPT_GROUP_IPC)) {
+        // completion = this member's last stream event and every peer's DONE, all queued on
+        // sW now: ckpt_wait then polls ONE stream (small snapshots are latency-bound)
+        CUDA_TRY(cudaStreamWaitEvent(c->sW, c->ev_done, 0));
+        if (c->m >= 2 && (rc = wait_all(c, c->sW, kDone, done_seq, 0))) return rc;
+        c->done_enqueued = true;
+    }
     return CKPT_OK;
 }
 
@@ -663,12 +673,21 @@ int sync_stream_timeout(ckpt_ctx *c, cudaStream_t s, const char *what) {
             cudaGetLastError();
             return fail(CKPT_EPEER, "%s: timed out after %.0f s waiting for peers (member %u: %s)", what, limit, c->me, buf);
         }
+        static const bool legacy = getenv("CKPT_WAIT_LEGACY") != nullptr;
+        if (el < 0.002 && !legacy) {  // the first 2 ms: poll without sleeping (small snapshots)
+            std::this_thread::yield();
+            continue;
+        }
         std::this_thread::sleep_for(std::chrono::microseconds(el < 0.01 ? 20 : 200));
     }
 }
 
 int wait_done_all(ckpt_ctx *c, uint32_t done_seq) {
     int rc;
+    if (c->done_enqueued) {  // see stage_finish
+        c->done_enqueued = false;
+        return sync_stream_timeout(c, c->sW, "wait");
+    }
     cudaStream_t ss[4] = {c->sP, c->sX, c->sC, c->sG};
     for (auto s : ss)
         if ((rc = sync_stream_timeout(c, s, "wait"))) return rc;
