@@ -23,6 +23,9 @@ def main():
     p.add_argument("--bucket", type=int, default=64 << 20)
     p.add_argument("--flags", type=int, default=0)
     p.add_argument("--with-d2h", action="store_true", help="run a pinned D2H on every device meanwhile")
+    p.add_argument("--rebuild", type=int, default=-1,
+                   help="then lose member k (device copy + host image) and rebuild it from the survivors' "
+                        "device images (Eq 2): rebuild kernel per launch, bytes and GB/s")
     a = p.parse_args()
     import torch
 
@@ -65,6 +68,38 @@ def main():
                       "xor_nvlink_gbs": st["xor_bytes_in"] / max(st["xor_ms"], 1e-9) / 1e6,
                       "pack_hbm_gbs": st["pack_bytes"] / max(st["pack_ms"], 1e-9) / 1e6,
                       "snapshot_ms": st["last_snapshot_ms"]}))
+    if a.rebuild >= 0:
+        k = a.rebuild
+        g = C.ckpt_geometry(ctxs[0])
+        for rep in range(2):
+            for c in ctxs:
+                C.ckpt_stats_reset(c)
+            C.ckpt_forget(ctxs[k], 0xA5)
+            torch.cuda.set_device(k)
+            for t in states[k][1]:
+                t.view(torch.uint8).fill_(0xA5)  # the lost member's tensors are gone too
+            for j, c in enumerate(ctxs):
+                torch.cuda.set_device(j)
+                C.ckpt_rebuild(c, k, torch.cuda.current_stream(j))
+            for j in range(m):
+                torch.cuda.synchronize(j)
+        rows = []
+        for j, c in enumerate(ctxs):
+            st = C.ckpt_get_stats(c)
+            if st["rebuild_launches"]:
+                rows.append({"member": j, "launches": st["rebuild_launches"],
+                             "kernel_us": round(st["rebuild_ms"] / st["rebuild_launches"] * 1e3, 2),
+                             "bytes_in": st["rebuild_bytes_in"], "bytes_out": st["rebuild_bytes_out"],
+                             "gbs_in_plus_out": round((st["rebuild_bytes_in"] + st["rebuild_bytes_out"])
+                                                      / max(st["rebuild_ms"], 1e-9) / 1e6, 1)})
+        # bit-exact: the lost member's tensors after a load equal the generator
+        from synth import SEED, fill as gfill
+        C.ckpt_load(ctxs[k], torch.cuda.current_stream(k))
+        torch.cuda.synchronize(k)
+        specs, ts = states[k]
+        ok = all(bool((ts[t].view(torch.uint8).cpu().numpy()[:4096] ==
+                       gfill(SEED, k, t, min(4096, specs[t].nbytes))).all()) for t in range(0, len(ts), 37))
+        print(json.dumps({"rebuild_lost": k, "m": m, "L_star": g["L_star"], "row_owners": rows, "sampled_ok": ok}))
     for c in ctxs:
         C.ckpt_destroy(c)
 
