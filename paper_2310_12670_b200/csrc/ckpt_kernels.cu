@@ -748,14 +748,18 @@ cudaError_t launch_pack_all(const PackAllArgs &a, int max_ctas, cudaStream_t s, 
             const char *e = getenv("CKPT_TMA_CFG");
             cfg = e ? atoi(e) : 4;
         }
-        // 64 short-lived CTAs per SM (each warp streams ~5 groups of 64 KiB) beat one
-        // persistent CTA per SM in the step: 6.48 vs 5.74 TB/s with the D2H running
-        // (CKPT_PACK_WAVES=k overrides; tools/pack_waves_ab.sh)
-        static int waves = -1;
-        if (waves < 0) {
+        // Short-lived CTAs (k per SM in the grid) beat one persistent CTA per SM in the step
+        // (tools/pack_waves_ab.sh, C2 rank, D2H running): k = 1: 5.74-5.86 TB/s, k = 8:
+        // 5.93-5.95 TB/s, k = 64: 6.46-6.50 TB/s -- but a co-running GEMM loses 1.0-2.3%
+        // at k = 8 against 2.3-3.7% at k = 64.  The snapshot pack (which a training GEMM may
+        // overlap) takes k = 8, the unpack of a load (recovery: nothing co-runs) k = 64;
+        // CKPT_PACK_WAVES=k overrides both.
+        static int waves_env = -1;
+        if (waves_env < 0) {
             const char *e = getenv("CKPT_PACK_WAVES");
-            waves = e ? std::max(1, atoi(e)) : 64;
+            waves_env = e ? std::max(1, atoi(e)) : 0;
         }
+        const int waves = waves_env ? waves_env : (a.unpack ? 64 : 8);
         const int ctas = (max_ctas / 2 > 0 ? max_ctas / 2 : 1) * waves;
         if (cfg == 2) return launch_pack_all_tma<6, 2>(a, ngroups, ctas, s);
         if (cfg == 1) return launch_pack_all_tma<8, 1>(a, ngroups, ctas, s);
