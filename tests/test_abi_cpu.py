@@ -194,3 +194,13 @@ def test_c_program_uses_the_abi(C, tmp_path):
     assert out["aor"] == "rc=0 w=" + ",".join(f"{x:08x}" for x in want)
     assert out["bad"].startswith("rc=-1 (invalid argument)")
     assert "sm_100a" in out["version"]
+
+
+def test_scripts_compile():
+    """bench.py, __graft_entry__.py and every tool parse (they run only on GPU boxes)."""
+    import glob
+    import py_compile
+    files = [os.path.join(ROOT, "bench.py"), os.path.join(ROOT, "__graft_entry__.py")] + \
+        sorted(glob.glob(os.path.join(ROOT, "tools", "*.py")))
+    for f in files:
+        py_compile.compile(f, doraise=True, cfile=os.devnull)
