@@ -198,9 +198,9 @@ def test_c_program_uses_the_abi(C, tmp_path):
 
 def test_scripts_compile():
     """bench.py, __graft_entry__.py and every tool parse (they run only on GPU boxes)."""
+    import ast
     import glob
-    import py_compile
     files = [os.path.join(ROOT, "bench.py"), os.path.join(ROOT, "__graft_entry__.py")] + \
         sorted(glob.glob(os.path.join(ROOT, "tools", "*.py")))
     for f in files:
-        py_compile.compile(f, doraise=True, cfile=os.devnull)
+        ast.parse(open(f).read(), filename=f)
