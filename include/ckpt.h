@@ -80,6 +80,11 @@ extern "C" {
 #define CKPT_OPT_WINDOWED    0x100u /* HAS placement (Alg 1, P.377-429): each bucket's D2H
                                       waits until the caller's training stream has opened
                                       the snapshot window (ckpt_window)                   */
+#define CKPT_OPT_REBUILD_SHARES 0x200u /* rebuild: the m-1 survivors each encode 1/(m-1) of
+                                      the lost member's parity row into its parity buffer
+                                      (reading Q27): the lost GPU receives L*.m/(m-1) instead
+                                      of 2.L* over NVLink.  Every member must agree (else
+                                      ckpt_protect returns EMISMATCH)                      */
 #define CKPT_OPT_SHM_ARENA   0x40u /* host arena in POSIX shared memory (/dev/shm), one file
                                       per member and host buffer: peers (ARC) and a restarted
                                       process can reach it; required by the ARC schemes     */
@@ -269,10 +274,13 @@ int ckpt_load(ckpt_ctx *ctx, void *stream);
  * host-blocking; every member passes the same lost_rank.  Survivors H2D their
  * completed data and parity, each row owner r != k XORs its parity with the other
  * survivors' units (NVLink reads) and writes the result into rank k's staging (P2P
- * stores); rank k re-encodes its parity row and D2Hs both into its completed image.
+ * stores); survivor i of the m-1 then encodes stripes [i*n/(m-1), (i+1)*n/(m-1)) of
+ * rank k's parity row (Eq 1 for row k: every term is a survivor's unit) into rank k's
+ * parity buffer (reading Q27; IPC: mapped from the handle rank k published in its flag
+ * page at ckpt_protect), and rank k D2Hs both into its completed image.
  * Follow with ckpt_load on every member to restore tensors.
  * Errors: EUNRECOVERABLE (m = 1, or a survivor has no completed image -- more than
- * one loss), EINVAL, ENOSNAP, ECUDA. */
+ * one loss), EINVAL, ENOSNAP, EPEER (rank k's parity handle cannot be mapped), ECUDA. */
 int ckpt_rebuild(ckpt_ctx *ctx, int32_t lost_rank, void *stream);
 
 /* REFT-load step 3 for up to two losses (P.545; collaborative protection P.507-508).

@@ -38,6 +38,7 @@ CKPT_OPT_DEVICE_ONLY = 0x20
 CKPT_OPT_SHM_ARENA = 0x40
 CKPT_OPT_HOST_LOAD = 0x80
 CKPT_OPT_WINDOWED = 0x100
+CKPT_OPT_REBUILD_SHARES = 0x200
 CKPT_SCHEME_DEFAULT, CKPT_SCHEME_AEC, CKPT_SCHEME_ARC, CKPT_SCHEME_ARC_AEC = 0, 1, 2, 3
 
 CKPT_DTYPE_BYTES, CKPT_DTYPE_BF16, CKPT_DTYPE_FP16, CKPT_DTYPE_FP32 = 0, 1, 2, 3

@@ -213,6 +213,7 @@ extern "C" int ckpt_destroy(ckpt_ctx *c) {
             if (c->peer_staging[j]) cudaIpcCloseMemHandle(c->peer_staging[j]);
             if (c->peer_flags[j]) cudaIpcCloseMemHandle(c->peer_flags[j]);
         }
+        if (c->peer_parity_opened[j]) cudaIpcCloseMemHandle(c->peer_parity[j]);
     }
     for (auto s : ss)
         if (s) cudaStreamDestroy(s);
@@ -392,6 +393,7 @@ extern "C" int ckpt_export_handle(ckpt_ctx *c, void *buf, uint64_t *len) {
     b.arena_key = c->opt.arena_key;
     b.attached_id = c->attached_id;
     gethostname(b.host, sizeof b.host - 1);
+    b.opt_flags = c->opt.flags;
     CUDA_TRY(cudaIpcGetMemHandle(&b.staging_h, c->staging));
     CUDA_TRY(cudaIpcGetMemHandle(&b.flags_h, c->flags));
     memset(buf, 0, CKPT_HANDLE_BYTES);
@@ -593,6 +595,8 @@ extern "C" int ckpt_protect(ckpt_ctx *c, const ckpt_group *g) {
         for (uint32_t j = 0; j < m; ++j) {
             if (hb[j]->arena_key != c->opt.arena_key)
                 return fail(CKPT_EMISMATCH, "protect: member %u uses another arena key", j);
+            if ((hb[j]->opt_flags ^ c->opt.flags) & CKPT_OPT_REBUILD_SHARES)
+                return fail(CKPT_EMISMATCH, "protect: members disagree on CKPT_OPT_REBUILD_SHARES (member %u)", j);
             c->group_version = std::max(c->group_version, hb[j]->attached_id);
         }
         for (uint32_t j = 0; j < m; ++j) {
@@ -632,6 +636,8 @@ extern "C" int ckpt_protect(ckpt_ctx *c, const ckpt_group *g) {
             if (!g->members[j]) return fail(CKPT_EINVAL, "protect: LOCAL group member %u is NULL", j);
             if (g->members[j]->opt.arena_key != c->opt.arena_key)
                 return fail(CKPT_EMISMATCH, "protect: member %u uses another arena key", j);
+            if ((g->members[j]->opt.flags ^ c->opt.flags) & CKPT_OPT_REBUILD_SHARES)
+                return fail(CKPT_EMISMATCH, "protect: members disagree on CKPT_OPT_REBUILD_SHARES (member %u)", j);
             c->group_version = std::max(c->group_version, g->members[j]->attached_id);
         }
         for (uint32_t j = 0; j < m; ++j) {
@@ -691,6 +697,11 @@ extern "C" int ckpt_protect(ckpt_ctx *c, const ckpt_group *g) {
     if (c->aec && cudaMalloc(&c->parity, c->parity_bytes) != cudaSuccess) {
         cudaGetLastError();
         return fail(CKPT_ENOMEM, "protect: parity buffer of %llu bytes failed", (unsigned long long)c->parity_bytes);
+    }
+    if (c->aec && c->transport == CKPT_GROUP_IPC) {  // published for a rebuild of this member
+        cudaIpcMemHandle_t h;
+        CUDA_TRY(cudaIpcGetMemHandle(&h, c->parity));
+        CUDA_TRY(cudaMemcpy((uint8_t *)c->flags + kParityHandleOff, &h, sizeof h, cudaMemcpyHostToDevice));
     }
     if (c->aec && (c->opt.flags & CKPT_OPT_CE_GATHER)) {
         c->gather_bytes = c->full_copy ? std::max<uint64_t>(Lstar, 4096) : c->parity_bytes * (m - 1);

@@ -70,6 +70,12 @@ constexpr uint64_t kFlagBytes = 4096;  // REL and DONE lines (READY line unused)
 constexpr uint32_t kMaxB = 16384;
 constexpr uint64_t kFlagAlloc = kFlagBytes + (uint64_t)CKPT_MAX_GROUP * kMaxB * 4;
 inline uint32_t *ready_row(uint32_t *flags, uint32_t j) { return flags + kFlagBytes / 4 + (uint64_t)j * kMaxB; }
+// IPC handle of the member's parity buffer, written into its own flag page by
+// ckpt_protect (the parity is allocated after the handle blobs were exchanged); a survivor
+// reads the lost member's copy there and maps it for the rebuild (rebuild_map_parity).
+constexpr uint64_t kParityHandleOff = 2048;
+static_assert(kNumStages * kFlagStride * 4 <= kParityHandleOff, "flag lines overlap the parity handle");
+static_assert(kParityHandleOff + sizeof(cudaIpcMemHandle_t) <= kFlagBytes, "parity handle beyond the flag page");
 
 struct HandleBlob {  // exported by ckpt_export_handle; fixed layout, <= CKPT_HANDLE_BYTES
     uint32_t magic, version;
@@ -85,6 +91,8 @@ struct HandleBlob {  // exported by ckpt_export_handle; fixed layout, <= CKPT_HA
     uint64_t arena_key;     // persistent arena key (0 = none); all members must agree
     uint64_t attached_id;   // committed snapshot id found in this member's persistent arena
     char host[64];
+    uint32_t opt_flags;     // CKPT_OPT_REBUILD_SHARES must agree
+    uint32_t reserved0;
     cudaIpcMemHandle_t staging_h;
     cudaIpcMemHandle_t flags_h;
 };
@@ -161,6 +169,9 @@ struct ckpt_ctx {
     uint8_t *peer_staging[CKPT_MAX_GROUP] = {};
     uint32_t *peer_flags[CKPT_MAX_GROUP] = {};
     bool peer_opened[CKPT_MAX_GROUP] = {};
+    uint8_t *peer_parity[CKPT_MAX_GROUP] = {};  // mapped on first rebuild of that member
+    bool peer_parity_opened[CKPT_MAX_GROUP] = {};
+    bool parity_peers_mapped = false;
     ckpt_ctx *members[CKPT_MAX_GROUP] = {};
 
     // CE gather buffer (CKPT_OPT_CE_GATHER; local): m-1 unit streams per bucket
@@ -263,10 +274,12 @@ static inline uint8_t *slot_ptr(const ckpt_ctx *c, uint8_t *base, uint64_t k) {
     return c->full_copy ? base + bucket_begin(c, k) : base + (uint64_t)(k % c->n_slots) * c->slot_bytes;
 }
 
-static inline uint8_t *parity_slot_ptr(const ckpt_ctx *c, uint64_t k) {
-    return c->full_copy ? c->parity + bucket_begin(c, k) / (c->m - 1)
-                        : c->parity + (uint64_t)(k % c->n_slots) * c->parity_slot_bytes;
+static inline uint8_t *parity_slot_ptr_at(const ckpt_ctx *c, uint8_t *parity, uint64_t k) {
+    return c->full_copy ? parity + bucket_begin(c, k) / (c->m - 1)
+                        : parity + (uint64_t)(k % c->n_slots) * c->parity_slot_bytes;
 }
+
+static inline uint8_t *parity_slot_ptr(const ckpt_ctx *c, uint64_t k) { return parity_slot_ptr_at(c, c->parity, k); }
 
 // Alg 1 placement of bucket k (ckpt_has_apply): the buckets that start below the split
 // go out only in bubbles; the others alongside computation -- or in a bubble, which is
@@ -340,6 +353,11 @@ int do_pack(ckpt_ctx *c, uint64_t k, uint8_t *slot, cudaStream_t s, bool unpack)
 int do_encode_range(ckpt_ctx *c, uint64_t k, uint64_t bb, uint64_t be, cudaStream_t s);
 int do_encode(ckpt_ctx *c, uint64_t k, cudaStream_t s);
 int do_rebuild_row(ckpt_ctx *c, uint64_t k, uint32_t kl, cudaStream_t s);
+int do_encode_lost_share(ckpt_ctx *c, uint64_t k, uint32_t kl, cudaStream_t s);
+int rebuild_map_parity(ckpt_ctx *c, uint32_t kl);
+// Without CKPT_OPT_REBUILD_SHARES the lost member re-encodes its own parity row (pulling
+// L* more over NVLink); with it the survivors encode it in shares (Q27)
+static inline bool rebuild_self_encode(const ckpt_ctx *c) { return !(c->opt.flags & CKPT_OPT_REBUILD_SHARES); }
 void clean_pad(ckpt_ctx *c, int buf);
 int check_sticky(ckpt_ctx *c);
 void make_sticky(ckpt_ctx *c, int rc);

@@ -205,6 +205,78 @@ int do_rebuild_row(ckpt_ctx *c, uint64_t k, uint32_t kl, cudaStream_t s) {
     return CKPT_OK;
 }
 
+// Re-encode lost rank kl's parity row (Eq 1 for row kl) on the survivors: every term of
+// row kl is a survivor's data unit sigma(kl, j), so survivor i (i-th of the m-1) XORs
+// stripes [s0, s1) of the bucket -- its own unit locally, m-2 over NVLink -- and stores
+// the result into kl's parity slot.  The lost GPU then receives L* of data + L*/(m-1) of
+// parity instead of pulling L* more to encode the row itself (reading Q27).
+int do_encode_lost_share(ckpt_ctx *c, uint64_t k, uint32_t kl, cudaStream_t s) {
+    const uint64_t bb = bucket_begin(c, k), be = bucket_end(c, k);
+    const uint64_t stripe = (uint64_t)(c->m - 1) * c->unit;
+    const uint64_t nst = (be - bb) / stripe;
+    const uint32_t i = c->me - (c->me > kl ? 1u : 0u);
+    const uint64_t s0 = nst * i / (c->m - 1), s1 = nst * (i + 1) / (c->m - 1);
+    if (s1 <= s0) return CKPT_OK;
+    if (!c->peer_parity[kl]) return fail(CKPT_ESTATE, "internal: parity of member %u not mapped", kl);
+    XorArgs a;
+    memset(&a, 0, sizeof a);
+    for (uint32_t j = 0; j < c->m; ++j) {
+        if (j == kl) continue;
+        XorTerm &t = a.in[a.nin++];
+        const uint64_t v = valid_in_bucket(c->peer_L[j], bb, be);
+        t.base = slot_ptr(c, c->peer_staging[j], k) + s0 * stripe;
+        t.valid = v > s0 * stripe ? v - s0 * stripe : 0;
+        t.stride = stripe;
+        t.off = (uint64_t)sigma(kl, j) * c->unit;
+    }
+    a.out = parity_slot_ptr_at(c, c->peer_parity[kl], k) + s0 * c->unit;
+    a.out_valid = UINT64_MAX;
+    a.out_stride = c->unit;
+    a.out_off = 0;
+    a.nstripes = s1 - s0;
+    a.unit = c->unit;
+    TimedLaunch *t;
+    int rc = timed_begin(c, s, 3, &t);
+    if (rc) return rc;
+    CUDA_TRY(launch_xor(a, c->xor_ctas, s));
+    rc = timed_end(t, s);
+    if (rc) return rc;
+    c->st.rebuild_launches++;
+    c->st.rebuild_bytes_in += (uint64_t)a.nin * (s1 - s0) * c->unit;
+    c->st.rebuild_bytes_out += (s1 - s0) * c->unit;
+    return CKPT_OK;
+}
+
+// Map lost member kl's parity buffer (survivors only): LOCAL members share the process;
+// IPC members read the handle kl published in its flag page at ckpt_protect.
+int rebuild_map_parity(ckpt_ctx *c, uint32_t kl) {
+    if (c->me == kl || c->peer_parity[kl]) return CKPT_OK;
+    if (c->transport == CKPT_GROUP_LOCAL) {
+        c->peer_parity[kl] = c->members[kl]->parity;
+        return c->peer_parity[kl] ? CKPT_OK : fail(CKPT_ESTATE, "rebuild: member %u has no parity buffer", kl);
+    }
+    cudaIpcMemHandle_t h;
+    memset(&h, 0, sizeof h);
+    cudaStream_t t = nullptr;  // non-blocking: must not wait for the training streams
+    CUDA_TRY(cudaStreamCreateWithFlags(&t, cudaStreamNonBlocking));
+    cudaError_t e = cudaMemcpyAsync(&h, (const uint8_t *)c->peer_flags[kl] + kParityHandleOff, sizeof h,
+                                    cudaMemcpyDeviceToHost, t);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(t);
+    cudaStreamDestroy(t);
+    if (e != cudaSuccess) return fail(CKPT_ECUDA, "rebuild: reading member %u's parity handle: %s", kl, cudaGetErrorString(e));
+    static const cudaIpcMemHandle_t zero = {};
+    if (!memcmp(&h, &zero, sizeof h)) return fail(CKPT_EPEER, "rebuild: member %u published no parity handle", kl);
+    void *p = nullptr;
+    e = cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        return fail(CKPT_EPEER, "rebuild: cudaIpcOpenMemHandle of member %u's parity: %s", kl, cudaGetErrorString(e));
+    }
+    c->peer_parity[kl] = (uint8_t *)p;
+    c->peer_parity_opened[kl] = true;
+    return CKPT_OK;
+}
+
 // ------------------------------------------------------------------ snapshot --------
 // The image's zero pad [L, L*) is structural (Q5) and never written by a D2H (which
 // covers [0, L)); after ckpt_forget poisoned a buffer, re-zero it before it commits.
@@ -735,6 +807,15 @@ extern "C" int ckpt_wait(ckpt_ctx *c, uint64_t id) {
     if (c->full_copy) c->staging_id = id;
     c->staging_poisoned = false;
     meta_commit(c);
+    // every peer has protected (its DONE for this snapshot arrived), so every parity
+    // handle is published: map them now, once, off the recovery path (a first
+    // cudaIpcOpenMemHandle of a multi-GB buffer costs tens of ms).  A failure here is
+    // left to the rebuild, which retries and reports it.
+    if (c->transport == CKPT_GROUP_IPC && c->aec && c->m >= 2 && !c->parity_peers_mapped && !rebuild_self_encode(c)) {
+        c->parity_peers_mapped = true;
+        for (uint32_t j = 0; j < c->m; ++j)
+            if (j != c->me && rebuild_map_parity(c, j)) cudaGetLastError();
+    }
     return CKPT_OK;
 }
 

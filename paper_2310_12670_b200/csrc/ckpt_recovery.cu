@@ -6,8 +6,9 @@ using namespace reft;
 // ------------------------------------------------------------------ rebuild ---------
 // Per bucket b (slot s), lost member kl:
 //   survivor j: C: [reuse: own kernel(b-n) done, REL(b-n) from all] H2D data+parity -> READY(b)
-//               X: own H2D, READY(b) from all -> rebuild row j into kl's slot -> REL(b)
-//   lost kl   : X: [reuse: own D2H(b-n)] READY(b) ; READY(b) from all -> encode row kl -> REL(b)
+//               X: own H2D, READY(b) from all -> rebuild row j into kl's slot, then encode
+//                  its share of kl's parity row into kl's parity slot -> REL(b)
+//   lost kl   : X: [reuse: own D2H(b-n)] READY(b) ; READY(b) from all -> REL(b)
 //               C: REL(b) from all, own encode -> D2H data + parity into its image
 int rb_stage1(ckpt_ctx *c, uint64_t b, uint32_t kl) {
     const uint32_t s = slot_of(c, b);
@@ -40,10 +41,10 @@ int rb_stage2(ckpt_ctx *c, uint64_t b, uint32_t kl) {
     int rc;
     if (c->me != kl) CUDA_TRY(cudaStreamWaitEvent(c->sX, c->ev_h2d[s], 0));
     if ((rc = wait_all(c, c->sX, kReady, bucket_seq(c, b), s))) return rc;
-    if (c->me != kl)
-        rc = do_rebuild_row(c, b, kl, c->sX);
-    else
-        rc = do_encode(c, b, c->sX);
+    if (rebuild_self_encode(c))
+        rc = c->me != kl ? do_rebuild_row(c, b, kl, c->sX) : do_encode(c, b, c->sX);
+    else if (c->me != kl && !(rc = do_rebuild_row(c, b, kl, c->sX)))
+        rc = do_encode_lost_share(c, b, kl, c->sX);
     if (rc) return rc;
     CUDA_TRY(cudaEventRecord(c->ev_kdone[s], c->sX));
     return sig_signal(c, c->sX, kRel, bucket_seq(c, b), s);
@@ -187,7 +188,7 @@ int rebuild_aec(ckpt_ctx *c, int32_t lost, void *stream) {
         }
         for (uint32_t j = 0; j < c->m; ++j) {
             ckpt_ctx *o = c->members[j];
-            if ((rc = set_dev(o)) || (rc = prepare_op(o, B))) goto bad;
+            if ((rc = set_dev(o)) || (!rebuild_self_encode(o) && (rc = rebuild_map_parity(o, kl))) || (rc = prepare_op(o, B))) goto bad;
             CUDA_TRY(cudaStreamWaitEvent(o->sC, o->ev_capture, 0));
             CUDA_TRY(cudaStreamWaitEvent(o->sX, o->ev_capture, 0));
         }
@@ -215,7 +216,7 @@ int rebuild_aec(ckpt_ctx *c, int32_t lost, void *stream) {
         return rc;
     }
     // IPC: every member runs its own side; the version is the survivors' completed id
-    if ((rc = prepare_op(c, B))) return rc;
+    if ((!rebuild_self_encode(c) && (rc = rebuild_map_parity(c, kl))) || (rc = prepare_op(c, B))) return rc;
     CUDA_TRY(cudaEventRecord(c->ev_capture, caller));
     CUDA_TRY(cudaStreamWaitEvent(c->sC, c->ev_capture, 0));
     CUDA_TRY(cudaStreamWaitEvent(c->sX, c->ev_capture, 0));

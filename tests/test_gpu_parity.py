@@ -118,6 +118,21 @@ def make_group(torch, C, m, unit, n_slots=0, bucket=1 << 20, flags=0, misalign=0
     return states, ctxs
 
 
+def test_rebuild_shares_flag_must_agree(torch, C):
+    """CKPT_OPT_REBUILD_SHARES changes who writes the lost member's parity row (Q27): a
+    group whose members disagree would leave it unwritten or written twice -> EMISMATCH."""
+    states = [tiny(j) for j in range(3)]
+    ctxs = [make_ctx(C, st, n_slots=0, bucket_bytes=1 << 20, flags=C.CKPT_OPT_REBUILD_SHARES if j == 1 else 0)
+            for j, st in enumerate(states)]
+    try:
+        with pytest.raises(C.CkptError) as e:
+            C.protect_local(ctxs)
+        assert e.value.code == C.CKPT_EMISMATCH
+    finally:
+        for c in ctxs:
+            C.ckpt_destroy(c)
+
+
 def snapshot_group(C, ctxs, bucket=0):
     ids = [C.ckpt_snapshot(c, bucket) for c in ctxs]
     for c, i in zip(ctxs, ids):
@@ -156,7 +171,10 @@ def test_group_encode_matches_oracle(torch, C, m, unit, n_slots, bucket, flags):
 @pytest.mark.parametrize("m,unit,n_slots,flags", [(2, 4096, 0, 0), (3, 4096, 2, 0), (4, 65536, 0, 0x2),
                                                   (8, 1024, 3, 0), (8, 0, 0, 0), (5, 64, 2, 0x2),
                                                   (4, 4096, 2, 0x18), (6, 256, 0, 0x18),
-                                                  (4, 65536, 0, 0x80), (3, 4096, 0, 0x82), (5, 4096, 0, 0x88)])
+                                                  (4, 65536, 0, 0x80), (3, 4096, 0, 0x82), (5, 4096, 0, 0x88),
+                                                  # CKPT_OPT_REBUILD_SHARES (Q27): survivors encode the lost row
+                                                  (2, 4096, 0, 0x200), (4, 4096, 2, 0x200), (5, 65536, 0, 0x202),
+                                                  (8, 1024, 3, 0x200), (3, 4096, 0, 0x280), (7, 16, 0, 0x200)])
 def test_group_drill_rebuild_every_rank(torch, C, m, unit, n_slots, flags):
     """Failure drill (Q12): rank k loses tensors and host image; rebuild + load."""
     from synth.gpu import fill_state
@@ -306,7 +324,7 @@ def test_c2_7b_tp8_rank_sampled(torch, C):
 
 
 @pytest.mark.parametrize("m,unit,flags", [(1, 65536, 0x20), (3, 4096, 0x20), (4, 65536, 0x22), (8, 1024, 0x28),
-                                          (5, 256, 0x30)])
+                                          (5, 256, 0x30), (4, 4096, 0x220), (6, 256, 0x230)])
 def test_device_only_drill(torch, C, m, unit, flags):
     """DEVICE_ONLY: the image and parity stay in HBM; every lost rank is rebuilt from
     the survivors' device images and reloaded bit-exactly."""

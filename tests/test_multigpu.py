@@ -135,6 +135,8 @@ def _world():
     ("tiny_6", 0, 0, 1 << 20, 0, 0),
     ("tiny_7", 4096, 2, 1 << 16, 0x18, 1),
     ("tiny_5", 256, 0, 1 << 20, 0x10, 0),
+    ("tiny_7", 4096, 0, 1 << 20, 0x200, 1),  # CKPT_OPT_REBUILD_SHARES (Q27)
+    ("tiny_5", 1024, 2, 1 << 16, 0x200, 0),
 ])
 def test_ipc_group_all_gpus(case):
     _run(min(_world(), 8), case)
