@@ -286,41 +286,107 @@ def test_c1_16mib_m8_full_parity(torch, C):
             C.ckpt_destroy(c)
 
 
-def test_c2_7b_tp8_rank_sampled(torch, C):
-    """BASELINE config 2 at full size on one GPU (m = 1, the N=1 bench launch
-    configuration): 1164 tensors, 11.8 GB.  Sampled check: head and tail of every
-    tensor's bytes in the host image vs the oracle's generator; load round trip on a
-    sample of tensors."""
-    from synth.gpu import make_rank_state, descriptors, fill_state
+BENCH_BUCKET = 512 << 20  # bench.py defaults: full-copy staging, 512 MiB buckets, TMA pack, u = 64 KiB
+
+
+def bench_options(C, **kw):
+    """The options bench.py's N=1 step runs with (bench.py main(): n_slots=0, 512 MiB
+    buckets, CKPT_OPT_TMA_PACK -> pack_all_tma_kernel, CKPT_OPT_HOST_LOAD for e2e's load)."""
+    o = dict(n_slots=0, bucket_bytes=BENCH_BUCKET, stripe_unit=64 << 10,
+             flags=C.CKPT_OPT_TIMING | C.CKPT_OPT_HOST_LOAD | C.CKPT_OPT_TMA_PACK)
+    o.update(kw)
+    return C.ckpt_options_default(**o)
+
+
+def test_c2_bench_config_full_image(torch, C):
+    """BASELINE config 2 at full size in EXACTLY the configuration bench.py times at N=1
+    (full-copy staging, 512 MiB buckets, the single-launch pack_all_tma_kernel, two host
+    buffers): 1164 tensors, 11.8 GB.  Unsampled: every byte of the committed host image
+    (both buffers, after the bench's warm-up pattern of repeated snapshots) against the
+    oracle's O3 (P.369-371), then every byte of every tensor after ckpt_load from the host
+    image (O7, P.545 step 1)."""
+    from gpu_util import verify_images_full, verify_tensors_full
+    from synth.gpu import make_rank_state, descriptors
     specs, ts = make_rank_state("c2_7b_tp8", 3, "cuda:0")
     assert len(specs) == 1164 and sum(s.nbytes for s in specs) == 11795488768
-    ctx = C.ckpt_create(0, C.ckpt_options_default(n_slots=4, bucket_bytes=64 << 20))
+    ctx = C.ckpt_create(0, bench_options(C, host_buffers=2))
     try:
         C.ckpt_register(ctx, descriptors(ts, specs))
-        sid = C.ckpt_snapshot(ctx)
-        C.ckpt_wait(ctx, sid)
-        data, _ = C.ckpt_host_view(ctx, 0)  # zero-copy view: slices are copied below
-        rng = np.random.default_rng(0)
-        for t, s in enumerate(specs):
-            off = C.ckpt_tensor_offset(ctx, t)
-            n = min(s.nbytes, 4096)
-            assert_bytes_equal(data[off:off + n].copy(), oracle.fill(synth.SEED, 3, t, n), f"tensor {t} head")
-            tail0 = s.nbytes - n
-            assert_bytes_equal(data[off + tail0:off + s.nbytes].copy(), oracle.fill(synth.SEED, 3, t, n, tail0),
-                               f"tensor {t} tail")
-            pad_end = C.ckpt_tensor_offset(ctx, t + 1) if t + 1 < len(specs) else data.size
-            assert not data[off + s.nbytes:pad_end].any()
-        del data
-        sample = rng.choice(len(specs), 6, replace=False)
-        fill_state(ts, 3, seed=1, xor_mode=1)
-        C.ckpt_load(ctx)
+        assert C.ckpt_protect(ctx, 1, 0) == C.CKPT_EUNAVAIL
+        stream = torch.cuda.current_stream()
+        Ls = C.ckpt_geometry(ctx)["L_star"]
+        for i in range(3):
+            sid = C.ckpt_snapshot(ctx, BENCH_BUCKET, stream)
+            C.ckpt_wait(ctx, sid)
+            if i == 0:
+                continue
+            st = C.ckpt_get_stats(ctx)
+            assert st["pack_launches"] == i + 1, "one pack launch per snapshot (single-launch TMA pack)"
+            d, _ = C.ckpt_host_view(ctx, 0)  # the buffer just committed (i = 1, 2: both buffers)
+            n = verify_images_full([specs], Ls, 65536, {0: (d, None)}, gen_ranks=[3])
+            assert n == Ls
+            del d
+        for t in ts:
+            t.view(torch.uint8).fill_(0xA5)
+        C.ckpt_load(ctx, stream)
         torch.cuda.synchronize()
-        for t in sample:
-            n = min(specs[t].nbytes, 1 << 20)
-            got = tensor_bytes(ts[t].view(torch.uint8)[:n])
-            assert_bytes_equal(got, oracle.fill(synth.SEED, 3, int(t), n), f"tensor {t} after load")
+        assert verify_tensors_full(specs, 3, ts) == sum(s.nbytes for s in specs)
     finally:
         C.ckpt_destroy(ctx)
+
+
+@pytest.mark.parametrize("m,k", [(2, 1), (3, 0), (4, 2)])
+def test_c2_group_full_image_and_rebuild(torch, C, m, k):
+    """BASELINE config 2 at full size as an m-member protection group on one device
+    (CKPT_GROUP_LOCAL: the same pack_all_tma_kernel and xor_tma_kernel<m-1> launches as the
+    one-process-per-GPU product, full-copy staging, 512 MiB buckets, one host buffer).
+    Unsampled: every byte of every member's data (O3) and parity row (O4, Eq 1 P.474-477)
+    against the oracle; then member k is lost (tensors and host image poisoned), rebuilt
+    (Eq 2 P.481-484) and every byte of its image compared with O6 and its parity row with
+    O4; finally every byte of its tensors after ckpt_load (P.545)."""
+    from gpu_util import verify_images_full, verify_tensors_full
+    from synth.gpu import make_rank_state, descriptors
+    free, _ = torch.cuda.mem_get_info()
+    need = m * (2 * 11795488768 + 11795890176 // (m - 1)) + (4 << 30)
+    if free < need:
+        pytest.skip(f"needs {need / 1e9:.0f} GB of HBM, {free / 1e9:.0f} free")
+    states, ctxs = [], []
+    try:
+        for j in range(m):
+            specs, ts = make_rank_state("c2_7b_tp8", j, "cuda:0")
+            states.append((specs, ts))
+            ctx = C.ckpt_create(0, bench_options(C, host_buffers=1))
+            ctxs.append(ctx)
+            C.ckpt_register(ctx, descriptors(ts, specs))
+        C.protect_local(ctxs)
+        stream = torch.cuda.current_stream()
+        ids = [C.ckpt_snapshot(c, BENCH_BUCKET, stream) for c in ctxs]
+        for c, i in zip(ctxs, ids):
+            C.ckpt_wait(c, i)
+        g = C.ckpt_geometry(ctxs[0])
+        Ls, u = g["L_star"], g["unit"]
+        all_specs = [sp for sp, _ in states]
+        views = {j: C.ckpt_host_view(ctxs[j], 0) for j in range(m)}
+        n = verify_images_full(all_specs, Ls, u, views)
+        assert n == m * (Ls + Ls // (m - 1))
+        del views
+        specs_k, ts_k = states[k]
+        C.ckpt_forget(ctxs[k], 0xA5)
+        for t in ts_k:
+            t.view(torch.uint8).fill_(0xA5)
+        for c in ctxs:
+            C.ckpt_rebuild(c, k, stream)
+        torch.cuda.synchronize()
+        views = {j: C.ckpt_host_view(ctxs[j], 0) for j in range(m)}
+        n = verify_images_full(all_specs, Ls, u, views, ranks=[k], rebuild_k=k)
+        assert n == Ls + Ls // (m - 1)
+        del views
+        C.ckpt_load(ctxs[k], stream)
+        torch.cuda.synchronize()
+        assert verify_tensors_full(specs_k, k, ts_k) == sum(s.nbytes for s in specs_k)
+    finally:
+        for c in ctxs:
+            C.ckpt_destroy(c)
 
 
 @pytest.mark.parametrize("m,unit,flags", [(1, 65536, 0x20), (3, 4096, 0x20), (4, 65536, 0x22), (8, 1024, 0x28),
