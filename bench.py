@@ -9,7 +9,8 @@ ongoing pinned host image -> commit on every rank (ckpt_snapshot + ckpt_wait).
 
 N = 1 runs snapshot only (a group of one has no redundancy); N >= 2 is launched under
 torchrun, one process per GPU, and the N ranks form one protection group (m = N).
-value = total state bytes committed by all ranks per second (GB/s, weak scaling).
+value = state bytes committed per GPU per second (GB/s per GPU, weak scaling); the
+aggregate over all N GPUs is `aggregate_gbs`.
 """
 from __future__ import annotations
 
@@ -43,6 +44,9 @@ def parse():
                    help="pack kernel: 128-bit LSU, TMA bulk through SMEM, or copy engines (zero SMs)")
     p.add_argument("--gather", default="kernel", choices=["kernel", "ce"],
                    help="parity: XOR kernel reads peers over NVLink, or copy engines pull units first")
+    p.add_argument("--encode", default="pull", choices=["pull", "push"],
+                   help="parity encode: pull (row owner reads its peers' units over NVLink) or push (every "
+                        "member XOR-reduces its units into the row owners' parity, CKPT_OPT_XOR_PUSH)")
     p.add_argument("--device-only", action="store_true",
                    help="CKPT_OPT_DEVICE_ONLY: device-side protect only (pack + parity into HBM, no D2H)")
     p.add_argument("--max-ctas", type=int, default=0, help="CTA budget of a pack/XOR launch (0 = 2 x SMs)")
@@ -104,38 +108,64 @@ class Clocks:
 
 
 # ------------------------------------------------------------------ CPU oracle ------
-def oracle_sample_threads(config: str, seconds: float, threads: int):
-    """The same single-rank oracle pack run on `threads` host threads at once, each on its own
-    slice of the workload's tensors (every thread calls the unchanged oracle; ctypes releases
-    the GIL), so the CPU baseline also uses the box's cores.  Returns (GB/s, description)."""
-    import threading
+class OracleGroup:
+    """The unchanged oracle on `threads` host threads at once for an m-member group: thread i
+    takes its own window of stripes of every member's image (windows cut through tensors;
+    a stripe-aligned window is exactly what O3/O4/O6 compute for those stripes) and runs
+    pack (O3) of every member, the parity of every row (O4) and the rebuild of member 0
+    (O6) on it.  Inputs are generated once, before any clock starts; run() times one pass."""
 
-    import oracle
-    import synth
+    def __init__(self, config: str, m: int, seconds: float, threads: int):
+        import bisect
 
-    specs = synth.config_tensors(config, 0)
-    budget = int(min(max(1.9e9 * seconds, 64 << 20), 4 << 30))  # bounded: generating it costs too
-    per = budget // threads
-    groups = [[] for _ in range(threads)]
-    acc = [0] * threads
-    t = 0
-    for k in range(threads):
-        while t < len(specs) and acc[k] < per:
-            n = min(specs[t].nbytes, per - acc[k])
-            groups[k].append(synth.fill(synth.SEED, 0, t, n))
-            acc[k] += n
-            t += 1
-    lays = [oracle.layout([x.size for x in gk]) for gk in groups]
-    th = [threading.Thread(target=oracle.pack, args=(gk, off, L)) for gk, (off, L) in zip(groups, lays)]
-    t0 = time.perf_counter()
-    for x in th:
-        x.start()
-    for x in th:
-        x.join()
-    dt = time.perf_counter() - t0
-    tot = sum(acc)
-    return tot / dt / 1e9, (f"oracle pack of {tot / 2**20:.0f} MiB of {config} rank 0, split over {threads} threads "
-                            f"(each the unchanged 1-thread oracle on its own tensors)")
+        import oracle
+        import synth
+
+        self.oracle, self.m, self.threads, self.u, self.config = oracle, m, threads, 65536, config
+        stripe = (m - 1) * self.u if m > 1 else 65536
+        specs = [synth.config_tensors(config, j) for j in range(m)]
+        nb = [[s_.nbytes for s_ in sp] for sp in specs]
+        offs = [oracle.layout(x)[0] for x in nb]
+        Lmin = min(oracle.layout(x)[1] for x in nb)
+        budget = int(min(max(0.6e9 * seconds * threads, 64 << 20), 4 << 30))  # state bytes, all members
+        W = max(stripe, budget // (threads * m) // stripe * stripe)
+        self.W = min(W, max(stripe, Lmin // threads // stripe * stripe))
+
+        def pieces(j, a_, b_):
+            ps, wh = [], []
+            t = max(0, bisect.bisect_right(offs[j], a_) - 1)
+            while t < len(nb[j]) and offs[j][t] < b_:
+                lo, hi = max(a_, offs[j][t]), min(b_, offs[j][t] + nb[j][t])
+                if lo < hi:
+                    ps.append(synth.fill(synth.SEED, j, t, hi - offs[j][t])[lo - offs[j][t]:])
+                    wh.append(lo - a_)
+                t += 1
+            return ps, wh
+
+        self.work = [[pieces(j, i * self.W, (i + 1) * self.W) for j in range(m)] for i in range(threads)]
+        self.state_bytes = self.W * m * threads
+        self.rebuilt_bytes = self.W * threads if m > 1 else 0
+        self.desc = (f"oracle pack{' + rotated XOR parity of every row + rebuild of member 0' if m > 1 else ''} of "
+                     f"{threads} windows x {self.W / 2**20:.0f} MiB of each of {m} member(s) of {config}, one "
+                     f"window per host thread ({threads} threads, each the unchanged 1-thread oracle)")
+
+    def run(self) -> float:
+        import threading
+        o, m, u = self.oracle, self.m, self.u
+
+        def one(i):
+            Ds = [o.pack(ps, wh, self.W) for ps, wh in self.work[i]]
+            if m > 1:
+                Ps = [o.encode(Ds, u, r) for r in range(m)]
+                o.rebuild([None] + Ds[1:], [None] + Ps[1:], u, 0, [True] + [False] * (m - 1))
+
+        th = [threading.Thread(target=one, args=(i,)) for i in range(self.threads)]
+        t0 = time.perf_counter()
+        for x in th:
+            x.start()
+        for x in th:
+            x.join()
+        return time.perf_counter() - t0
 
 
 def oracle_sample(config: str, m: int, seconds: float, step_seed: int = 0):
@@ -182,25 +212,28 @@ def oracle_sample(config: str, m: int, seconds: float, step_seed: int = 0):
 
 
 def reference_arm(a, rank, world):
+    """The oracle as it stands, on every host core (one window of stripes per thread), for the
+    same workload and group size as our arm: one step = pack (O3) of every member + parity
+    of every row (O4) + rebuild of member 0 (O6) on a bounded sample (inputs generated once,
+    before the clock).  value = state GB/s per member (the group's rate / m), the unit of our
+    arm's per-GPU value."""
     if rank != 0:
         return 0
     m = max(world, a.gpus)
-    vals, descs = [], None
-    per = max(a.cpu_seconds / max(a.steps, 1), 2.0)
-    for i in range(a.warmup):
-        oracle_sample(a.config, m, min(per, 2.0), step_seed=i)
-    t_all, b_all = 0.0, 0
-    for i in range(a.steps):
-        gbs, descs, tot, dt = oracle_sample(a.config, m, per, step_seed=100 + i)
-        vals.append(gbs)
-        t_all += dt
-        b_all += tot
-    value = b_all / t_all / 1e9
+    nthr = os.cpu_count() or 1
+    og = OracleGroup(a.config, m, max(a.cpu_seconds / max(a.steps, 1), 1.0), nthr)
+    for _ in range(a.warmup):
+        og.run()
+    t_all = sum(og.run() for _ in range(a.steps))
+    value = og.state_bytes * a.steps / t_all / 1e9 / m
     line = {"impl": "reference", "metric": METRIC, "value": round(value, 4), "unit": "GB/s", "n_gpus": m,
             "steps": a.steps, "warmup": a.warmup, "ms_per_step": round(t_all / a.steps * 1e3, 3),
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u8", "data": "synthetic",
-            "config": {"workload": a.config, "m": m, "sample": descs},
-            "cpu_baseline": {"value": round(value, 4), "unit": "GB/s", "cores": 1, "kind": "oracle", "sample": descs},
+            "config": {"workload": a.config, "m": m, "sample": og.desc,
+                       "same_config": "same workload and m as our arm; a bounded window of every member per step"},
+            "aggregate_gbs": round(value * m, 4),
+            "cpu_baseline": {"value": round(value, 4), "unit": "GB/s", "cores": nthr, "kind": "oracle",
+                             "sample": og.desc},
             "e2e": {"value": round(value, 4), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
     return 0
@@ -256,7 +289,7 @@ def main():
     flags = (C.CKPT_OPT_TIMING | C.CKPT_OPT_HOST_LOAD | (C.CKPT_OPT_TMA_PACK if a.pack == "tma" else 0)
              | (C.CKPT_OPT_LSU_PACK if a.pack == "lsu" else 0)
              | (C.CKPT_OPT_CE_PACK if a.pack == "ce" else 0) | (C.CKPT_OPT_CE_GATHER if a.gather == "ce" else 0)
-             | (C.CKPT_OPT_DEVICE_ONLY if a.device_only else 0))
+             | (C.CKPT_OPT_DEVICE_ONLY if a.device_only else 0) | (C.CKPT_OPT_XOR_PUSH if a.encode == "push" else 0))
     if a.device_only:
         a.n_slots = 0
     # pinned host arena per rank and buffer: L + L/(m-1) (AEC) [+ the ARC copy of the
@@ -324,6 +357,25 @@ def main():
     del db
     hb.release()
 
+    # NVLink roofline, measured live (N >= 2, protected): every member pulls from all of its
+    # m-1 peers at once -- the encode's all-to-all pattern -- with the XOR kernel's own bulk
+    # load mechanism (SM) and with copy engines (CE); best of 3, barrier-aligned
+    fabric = None
+    if m >= 2 and scheme != C.CKPT_SCHEME_ARC:
+        per_peer = min(1 << 30, (g["L"] // (m - 1)) // 16384 * 16384)
+        fabric = {"bytes_per_peer": per_peer}
+        for name, mode in (("sm_pull", C.CKPT_PROBE_SM_PULL), ("ce_pull", C.CKPT_PROBE_CE_PULL)):
+            vals = []
+            for _ in range(3):
+                barrier()
+                torch.cuda.synchronize()
+                vals.append(C.ckpt_probe_fabric(ctx, mode, per_peer, 0, stream))
+            fabric[name + "_gbs_rank0"] = round(max(vals), 1)
+            fabric[name + "_gbs_min_over_ranks"] = round(-allmax(-max(vals)), 1)
+        fabric["note"] = ("ckpt_probe_fabric: all members pull bytes_per_peer from each of their m-1 peers at "
+                          "once; sm_pull = cp.async.bulk loads on the XOR kernel's CTA budget (its roofline), "
+                          "ce_pull = one copy-engine copy per peer")
+
     def step():
         sid = C.ckpt_snapshot(ctx, a.bucket, stream)
         C.ckpt_wait(ctx, sid)
@@ -346,7 +398,8 @@ def main():
     t_ms = allmax(e0.elapsed_time(e1))
     st = C.ckpt_get_stats(ctx)
     total_state = allsum(S) * a.steps
-    value = total_state / (t_ms / 1e3) / 1e9
+    aggregate = total_state / (t_ms / 1e3) / 1e9
+    value = aggregate / N  # the metric is GB/s PER GPU (weak scaling: every GPU snapshots its own shard)
     wire = st["d2h_bytes"] / (e0.elapsed_time(e1) / 1e3) / 1e9  # this rank's host-link GB/s
 
     # dominant kernel roofline (launch durations timed with events on its stream)
@@ -364,14 +417,20 @@ def main():
                                              "bytes_per_launch": per, "avg_launch_us": dur * 1e3,
                                              "launches": st["pack_launches"],
                                              "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy r+w)"}))
-    xor_name = "xor_kernel<m-1>" if os.environ.get("CKPT_XOR_IMPL") == "lsu" else "xor_tma_kernel<m-1>"
+    xor_name = ("xor_push_kernel" if a.encode == "push" else
+                "xor_kernel<m-1>" if os.environ.get("CKPT_XOR_IMPL") == "lsu" else "xor_tma_kernel<m-1>")
     if st["xor_launches"] and a.gather == "kernel":
         per = st["xor_bytes_in"] / st["xor_launches"]
         dur = st["xor_ms"] / st["xor_launches"]
-        kern.append(("xor", st["xor_ms"], {"bound": "nvlink", "achieved": per / dur / 1e6, "peak": NVLINK_PEAK_GBS,
+        live = fabric.get("sm_pull_gbs_min_over_ranks") if fabric else None
+        kern.append(("xor", st["xor_ms"], {"bound": "nvlink", "achieved": per / dur / 1e6,
+                                           "peak": live or NVLINK_PEAK_GBS,
                                            "unit": "GB/s", "kernel": xor_name, "bytes_per_launch": per,
                                            "avg_launch_us": dur * 1e3, "launches": st["xor_launches"],
-                                           "peak_source": "B200_PROFILING.md measured peer copy 770 GB/s/direction"}))
+                                           "frac_of_770": round(per / dur / 1e6 / NVLINK_PEAK_GBS, 4),
+                                           "peak_source": ("live all-concurrent NVLink pull probe (ckpt_probe_fabric "
+                                                           "sm_pull, min over ranks), this run" if live else
+                                                           "B200_PROFILING.md measured peer copy 770 GB/s/direction")}))
     elif st["xor_launches"]:  # CE gather: the XOR kernel reads local HBM (m-1 streams) and writes parity
         per = (st["xor_bytes_in"] + st["xor_bytes_out"]) / st["xor_launches"]
         dur = st["xor_ms"] / st["xor_launches"]
@@ -383,10 +442,23 @@ def main():
     roof = kern[0][2] if kern else None
     if roof:
         roof["frac"] = roof["achieved"] / roof["peak"]
-        tr_path = os.path.join(ROOT, "profiles", f"traffic_{roof['kernel'].split('<')[0]}_{a.config}.json")
-        roof["traffic"] = json.load(open(tr_path)).get("bytes_per_launch") if os.path.exists(tr_path) else None
+        # per-launch traffic from one ncu capture of this kernel, config AND group size m;
+        # for the NVLink-bound XOR it is the NVLink receive user bytes (nvlrx__bytes_data_user),
+        # for the HBM-bound pack DRAM read + write; null when no capture exists for this m
+        tr_path = os.path.join(ROOT, "profiles", f"traffic_{roof['kernel'].split('<')[0]}_{a.config}_m{m}.json")
+        tr = json.load(open(tr_path)) if os.path.exists(tr_path) else {}
+        roof["traffic"] = tr.get("bytes_per_launch")
+        roof["traffic_metric"] = tr.get("metric")
+        roof["traffic_source"] = os.path.relpath(tr_path, ROOT) if tr else None
         for k in ("achieved", "frac", "avg_launch_us"):
             roof[k] = round(roof[k], 4)
+    # E9 analog (P.469: erasure coding at 12-15x the snapshot rate): the XOR encode's
+    # in-situ NVLink GB/s over this rank's host-link (D2H wire) GB/s
+    e9 = None
+    xk = [d for k, _, d in kern if k == "xor"]
+    if xk and wire > 0:
+        e9 = {"value": round(xk[0]["achieved"] / wire, 2), "xor_gbs": round(xk[0]["achieved"], 1),
+              "d2h_wire_gbs": round(wire, 2), "paper": "12-15x (P.469)"}
     others = {k: {kk: (round(vv, 4) if isinstance(vv, float) else vv) for kk, vv in d.items()} for k, _, d in kern[1:]}
     launches = int(allsum(st["pack_launches"] + st["xor_launches"]))
 
@@ -406,7 +478,7 @@ def main():
         barrier()
         te = allmax(time.perf_counter() - t0)
         st2 = C.ckpt_get_stats(ctx)
-        e2e = {"value": round(allsum(S) * a.steps / te / 1e9, 4), "unit": "GB/s",
+        e2e = {"value": round(allsum(S) * a.steps / te / 1e9 / N, 4), "unit": "GB/s (per GPU)",
                "h2d_bytes_per_step": int(st2["h2d_bytes"] // a.steps),
                "d2h_bytes_per_step": int(st2["d2h_bytes"] // a.steps),
                "what": "ckpt_load (restore from the completed host image) + ckpt_snapshot + ckpt_wait per step, "
@@ -432,19 +504,28 @@ def main():
             C.ckpt_protect(ctx2, 1, 0)
         corun["ce_pack"] = gemm_corun(torch, C, ctx2, stream, a.bucket, barrier, allmax, dev)
         C.ckpt_destroy(ctx2)
-    if corun:  # the better of the two library configurations, named (both are reported)
-        best = min(corun, key=lambda k: corun[k]["slowdown_pct"])
-        corun["slowdown_pct"] = corun[best]["slowdown_pct"]
-        corun["slowdown_pct_config"] = best
+    if corun:  # headline: the configuration whose throughput is the headline (both reported)
+        corun["slowdown_pct"] = corun["this_config"]["slowdown_pct"]
+        corun["slowdown_pct_config"] = "this_config"
 
     cpu = None
     if rank == 0 and world == 1 and not a.no_cpu_baseline:
         gbs, desc, _, _ = oracle_sample(a.config, 1, a.cpu_seconds)
         cpu = {"value": round(gbs, 4), "unit": "GB/s", "cores": 1, "kind": "oracle", "sample": desc}
         nthr = os.cpu_count() or 1
-        gbs_t, desc_t = oracle_sample_threads(a.config, min(a.cpu_seconds, 10.0), nthr)
-        cpu["all_cores"] = {"value": round(gbs_t, 4), "unit": "GB/s", "cores": nthr, "kind": "oracle",
-                            "sample": desc_t}
+        og = OracleGroup(a.config, 1, min(a.cpu_seconds, 8.0), nthr)
+        dt = og.run()
+        cpu["all_cores"] = {"value": round(og.state_bytes / dt / 1e9, 4), "unit": "GB/s", "cores": nthr,
+                            "kind": "oracle", "sample": og.desc}
+        # the oracle's encode and rebuild (O4, O6) on all cores for a 4-member group: the
+        # host-side counterpart of the parity work a protected N >= 2 step does
+        og = OracleGroup(a.config, 4, min(a.cpu_seconds, 8.0), nthr)
+        dt = og.run()
+        cpu["parity_all_cores_m4"] = {"value": round(og.state_bytes / dt / 1e9 / 4, 4),
+                                      "unit": "GB/s per member", "group_gbs": round(og.state_bytes / dt / 1e9, 4),
+                                      "rebuild_gbs": round(og.rebuilt_bytes / dt / 1e9, 4), "cores": nthr,
+                                      "kind": "oracle", "sample": og.desc}
+        del og
 
     if rank == 0:
         line = {
@@ -453,11 +534,13 @@ def main():
             "scaling": "weak", "vs_baseline": None, "dtype": "u8", "data": "synthetic",
             "config": {"workload": a.config, "state_bytes_per_gpu": S, "tensors_per_gpu": len(specs),
                        "m": m, "L_star": g["L_star"], "stripe_unit": g["unit"], "bucket_bytes": a.bucket,
-                       "n_slots": a.n_slots, "pack": a.pack, "gather": a.gather, "device_only": a.device_only,
+                       "n_slots": a.n_slots, "pack": a.pack, "gather": a.gather, "encode": a.encode, "device_only": a.device_only,
                        "max_ctas": a.max_ctas or "2 x SMs", "host_buffers": host_buffers,
                        "scheme": a.scheme, "groups": f"{world // (a.group_size or world)} x m={a.group_size or world}",
                        "l2": f"inputs {S / 1e9:.2f} GB/GPU >> 126 MB L2; no flush needed"},
-            "per_gpu_gbs": round(value / N, 3),
+            "aggregate_gbs": round(aggregate, 3),
+            "fabric": fabric,
+            "e9_ratio": e9,
             "host_link": None if a.device_only else {
                 "achieved_wire_gbs_rank0": round(wire, 3), "peak_d2h_gbs_rank0_measured": round(d2h_peak, 3),
                 "frac": round(wire / d2h_peak, 4), "note": "binding roofline of the whole step: pinned D2H of data + parity"},
@@ -507,14 +590,18 @@ def registered_host_buffer(torch, n):
     return _Registered(torch, n)
 
 
-def gemm_corun(torch, C, ctx, stream, bucket, barrier, allmax, dev):
-    """bf16 8192^3 GEMMs back to back on a HIGH-priority stream; slowdown while a
-    snapshot runs on the library's low-priority streams.  Interleaved A/B x3."""
+def gemm_corun(torch, C, ctx, stream, bucket, barrier, allmax, dev, pairs=10):
+    """bf16 8192^3 GEMMs back to back on a HIGH-priority stream; slowdown while a snapshot
+    runs on the library's low-priority streams (the O_in-mem analog, P.234-236; HAS Layer 2,
+    P.423).  `pairs` interleaved A/B windows (alone, with snapshot), each >= 1.5x a snapshot.
+    Every GEMM is bracketed by its own CUDA events, so besides the whole window the slowdown
+    is also reported over the GEMMs that overlap the pack kernel (the pack window) and the
+    device-side protect (pack + XOR), located relative to an event recorded on the caller
+    stream at the snapshot's capture point.  Times are max over ranks per window."""
     n = 8192
     A = torch.randn(n, n, dtype=torch.bfloat16, device=dev)
     Bm = torch.randn(n, n, dtype=torch.bfloat16, device=dev)
     hi = torch.cuda.Stream(device=dev, priority=-5)
-    # size the GEMM window to ~1.5x one snapshot
     with torch.cuda.stream(hi):
         for _ in range(3):
             torch.matmul(A, Bm)
@@ -531,39 +618,71 @@ def gemm_corun(torch, C, ctx, stream, bucket, barrier, allmax, dev):
     C.ckpt_wait(ctx, sid)
     snap_ms = C.ckpt_get_stats(ctx)["last_snapshot_ms"] or 250.0
     iters = int(allmax(int(max(20, 1.5 * snap_ms / per))))
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(iters)]
 
     def window(with_snap):
         barrier()
         torch.cuda.synchronize()
-        s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        es = torch.cuda.Event(enable_timing=True)
         sid = None
+        st0 = C.ckpt_get_stats(ctx)
+        es.record(stream)
         if with_snap:
             sid = C.ckpt_snapshot(ctx, bucket, stream)
-        s0.record(hi)
         with torch.cuda.stream(hi):
-            for _ in range(iters):
+            for g0, g1 in ev:
+                g0.record(hi)
                 torch.matmul(A, Bm)
-        s1.record(hi)
+                g1.record(hi)
         if sid is not None:
             C.ckpt_wait(ctx, sid)
-        s1.synchronize()
-        snap = C.ckpt_get_stats(ctx)["last_snapshot_ms"] if with_snap else None
-        return allmax(s0.elapsed_time(s1)), snap
+        ev[-1][1].synchronize()
+        st1 = C.ckpt_get_stats(ctx)
+        total = ev[0][0].elapsed_time(ev[-1][1])
+        spans = [(es.elapsed_time(g0), es.elapsed_time(g1)) for g0, g1 in ev]
+        pack = (st1["pack_ms"] - st0["pack_ms"]) / max(1, st1["pack_launches"] - st0["pack_launches"]) \
+            if st1["pack_launches"] > st0["pack_launches"] else 0.0
+        xor = (st1["xor_ms"] - st0["xor_ms"]) if st1["xor_launches"] > st0["xor_launches"] else 0.0
+        snap = st1["last_snapshot_ms"] if with_snap else None
+        return allmax(total), spans, pack, xor, snap
 
-    alone, withs, snaps = [], [], []
-    for _ in range(5):
-        alone.append(window(False)[0])
-        w, s = window(True)
-        withs.append(w)
-        snaps.append(s)
-    ta, tw = statistics.median(alone), statistics.median(withs)
+    def overlap_mean(spans, lo, hi_):
+        d = [b - a for a, b in spans if b > lo and a < hi_]
+        return (sum(d) / len(d), len(d)) if d else (None, 0)
+
+    rows = []
+    for _ in range(pairs):
+        ta, sa, _, _, _ = window(False)
+        tw, sw, pack, xor, snap = window(True)
+        base = sum(b - a for a, b in sa[2:]) / max(1, len(sa) - 2)  # per-GEMM time alone (warm)
+        pw, npw = overlap_mean(sw, 0.0, pack)
+        dw, ndw = overlap_mean(sw, 0.0, pack + xor)
+        sn, nsn = overlap_mean(sw, 0.0, snap or 0.0)
+        rows.append({"whole_pct": (tw / ta - 1) * 100,
+                     "pack_window_pct": (pw / base - 1) * 100 if pw else None, "pack_window_gemms": npw,
+                     "protect_window_pct": (dw / base - 1) * 100 if dw else None,
+                     "snapshot_window_pct": (sn / base - 1) * 100 if sn else None,
+                     "alone_ms": ta, "with_ms": tw, "pack_ms": pack, "xor_ms": xor, "snapshot_ms": snap})
+
+    def summ(key):
+        v = [r[key] for r in rows if r[key] is not None]
+        if not v:
+            return None
+        return {"median": round(statistics.median(v), 3), "min": round(min(v), 3), "max": round(max(v), 3),
+                "spread": round(max(v) - min(v), 3)}
+
     flops = 2 * n ** 3 * iters
-    return {"slowdown_pct": round((tw / ta - 1) * 100, 3), "gemm_ms_alone": round(ta, 3),
-            "gemm_ms_with_snapshot": round(tw, 3), "gemm_iters": iters,
-            "gemm_tflops_alone": round(flops / ta / 1e9, 1),
-            "snapshot_ms_while_corunning": round(statistics.median(snaps), 3),
+    whole = summ("whole_pct")
+    return {"slowdown_pct": whole["median"], "whole_window": whole,
+            "pack_window": summ("pack_window_pct"), "protect_window": summ("protect_window_pct"),
+            "snapshot_window": summ("snapshot_window_pct"),
+            "pairs": [{k: (round(v, 3) if isinstance(v, float) else v) for k, v in r.items()} for r in rows],
+            "gemm_iters": iters, "gemm_tflops_alone": round(flops / statistics.median([r["alone_ms"] for r in rows]) / 1e9, 1),
             "snapshot_ms_alone": round(snap_ms, 3),
-            "window": "whole GEMM window (>= 1.5x snapshot), median of 5 interleaved A/B, max over ranks"}
+            "window": (f"{pairs} interleaved A/B pairs; whole = GEMM window (>= 1.5x snapshot, max over ranks); "
+                       "pack / protect / snapshot window = mean per-GEMM time of the GEMMs overlapping "
+                       "[capture, +pack] / [capture, +pack+xor] / [capture, +snapshot] vs the warm per-GEMM "
+                       "time alone (this rank)")}
 
 
 if __name__ == "__main__":

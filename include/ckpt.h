@@ -85,6 +85,14 @@ extern "C" {
                                       (reading Q27): the lost GPU receives L*.m/(m-1) instead
                                       of 2.L* over NVLink.  Every member must agree (else
                                       ckpt_protect returns EMISMATCH)                      */
+#define CKPT_OPT_XOR_PUSH    0x400u /* parity encode in push mode (full-copy staging only;
+                                      otherwise ignored): every member sends each unit of its
+                                      own image to its row owner as a bulk XOR reduction
+                                      (cp.reduce.async.bulk .xor) into that owner's parity,
+                                      which the owner zeroes before its pack -- posted NVLink
+                                      writes instead of round-trip peer reads.  Same bytes as
+                                      the pull encode (Eq 1).  Every member must agree (else
+                                      ckpt_protect returns EMISMATCH)                      */
 #define CKPT_OPT_SHM_ARENA   0x40u /* host arena in POSIX shared memory (/dev/shm), one file
                                       per member and host buffer: peers (ARC) and a restarted
                                       process can reach it; required by the ARC schemes     */
@@ -377,6 +385,26 @@ typedef struct ckpt_has_plan_t {
 } ckpt_has_plan_t;
 int ckpt_has_plan(uint32_t stage, uint32_t num_stages, double c_fb_bp_s, uint64_t snapshot_bytes,
                   double b_io_bytes_per_s, ckpt_has_plan_t *out);
+
+/* ---- fabric probe (measurement; "NVLink ... to be measured P2P, all
+ * ranks concurrent") --------------------------------------------------------------------
+ * Every member of a protected group reads `bytes_per_peer` bytes from EACH of its m-1
+ * peers' device staging at once: the encode's all-to-all pattern (row r pulls L* /(m-1)
+ * from every peer, Eq 1 P.474-477), so the result is the denominator of the XOR kernel's
+ * roofline.  mode CKPT_PROBE_SM_PULL: the XOR kernel's own load mechanism (cp.async.bulk
+ * peer -> SMEM, 16 KiB pieces, 3 stages per warp, data discarded) on `ctas` CTAs (0 = the
+ * XOR kernel's CTA budget); CKPT_PROBE_CE_PULL: one copy-engine cudaMemcpyAsync per peer,
+ * each on its own stream, into a scratch buffer the call allocates and frees.
+ * Read-only: no staging or image is modified.  Not a collective protocol, but every member
+ * must call it at the same time for the figure to mean anything (the caller aligns them,
+ * e.g. with a barrier).  *gbs = bytes_per_peer * (m-1) / elapsed time between CUDA events
+ * on `stream` (host-synchronous: returns after the copies finished).
+ * Errors: EINVAL (bytes_per_peer 0, not a multiple of 16 KiB, or beyond a peer's staging),
+ * ESTATE (not protected, m < 2, or a snapshot in flight), ECUDA. */
+#define CKPT_PROBE_SM_PULL 0
+#define CKPT_PROBE_CE_PULL 1
+int ckpt_probe_fabric(ckpt_ctx *ctx, int mode, uint64_t bytes_per_peer, uint32_t ctas, void *stream,
+                      double *gbs);
 
 /* Library version string, e.g. "reft-ckpt 0.1 sm_100a". */
 const char *ckpt_version(void);

@@ -21,7 +21,7 @@ FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O2,-Wall,-fvisi
          "-Xptxas", "-v", "-I" + os.path.join(ROOT, "include")]
 
 LIBS = {
-    "libreft_ckpt.so": ["ckpt_api.cu", "ckpt_hostmem.cu", "ckpt_pipeline.cu", "ckpt_recovery.cu", "ckpt_kernels.cu",
+    "libreft_ckpt.so": ["ckpt_api.cu", "ckpt_hostmem.cu", "ckpt_pipeline.cu", "ckpt_recovery.cu", "ckpt_kernels.cu", "ckpt_probe.cu",
                         "ckpt_aor.cu", "aor_update.cpp"],
     "libreft_synth.so": ["synth_fill.cu"],
 }

@@ -39,6 +39,8 @@ CKPT_OPT_SHM_ARENA = 0x40
 CKPT_OPT_HOST_LOAD = 0x80
 CKPT_OPT_WINDOWED = 0x100
 CKPT_OPT_REBUILD_SHARES = 0x200
+CKPT_OPT_XOR_PUSH = 0x400
+CKPT_PROBE_SM_PULL, CKPT_PROBE_CE_PULL = 0, 1
 CKPT_SCHEME_DEFAULT, CKPT_SCHEME_AEC, CKPT_SCHEME_ARC, CKPT_SCHEME_ARC_AEC = 0, 1, 2, 3
 
 CKPT_DTYPE_BYTES, CKPT_DTYPE_BF16, CKPT_DTYPE_FP16, CKPT_DTYPE_FP32 = 0, 1, 2, 3
@@ -158,6 +160,7 @@ def lib():
             "ckpt_plan_common": (ctypes.c_int, [_vp, _u32, _u64, ctypes.POINTER(_u64), ctypes.POINTER(_u64)]),
             "ckpt_version": (ctypes.c_char_p, []),
             "ckpt_arena_unlink": (ctypes.c_int, [_u64, _u32, _u32]),
+            "ckpt_probe_fabric": (ctypes.c_int, [_vp, ctypes.c_int, _u64, _u32, _vp, ctypes.POINTER(ctypes.c_double)]),
             # include/ckpt_aor.h
             "ckpt_aor_options_default": (None, [ctypes.POINTER(ckpt_aor_options)]),
             "ckpt_aor_create": (ctypes.c_int, [ctypes.c_int, ctypes.POINTER(ckpt_aor_options),
@@ -345,6 +348,14 @@ def ckpt_has_plan(stage: int, num_stages: int, c_fb_bp_s: float, snapshot_bytes:
 
 def ckpt_sync(ctx: int) -> None:
     _check(lib().ckpt_sync(ctx), "ckpt_sync")
+
+
+def ckpt_probe_fabric(ctx: int, mode: int, bytes_per_peer: int, ctas: int = 0, stream=None) -> float:
+    """All-concurrent NVLink pull GB/s of this member (every member must call it at once)."""
+    g = ctypes.c_double()
+    _check(lib().ckpt_probe_fabric(ctx, mode, bytes_per_peer, ctas, _stream_handle(stream), ctypes.byref(g)),
+           "ckpt_probe_fabric")
+    return g.value
 
 
 def ckpt_forget(ctx: int, poison: int = 0xA5) -> None:

@@ -174,6 +174,7 @@ extern "C" int ckpt_create(int device, const ckpt_options *o, ckpt_ctx **out) {
     // measured: at m = 2 half the SMs read peers as fast as 2 x SMs (660 vs 671 GB/s), at
     // m = 4 they do not (497 vs 590 GB/s) -- the XOR keeps the full budget
     c->xor_ctas = c->max_ctas;
+    if (const char *x = getenv("CKPT_XOR_CTAS"); x && atoi(x) > 0) c->xor_ctas_push = atoi(x);
     int least = 0, greatest = 0;
     cudaDeviceGetStreamPriorityRange(&least, &greatest);
     int prio = opt.priority == INT32_MAX ? least : std::min(least, std::max(greatest, (int)opt.priority));
@@ -595,8 +596,8 @@ extern "C" int ckpt_protect(ckpt_ctx *c, const ckpt_group *g) {
         for (uint32_t j = 0; j < m; ++j) {
             if (hb[j]->arena_key != c->opt.arena_key)
                 return fail(CKPT_EMISMATCH, "protect: member %u uses another arena key", j);
-            if ((hb[j]->opt_flags ^ c->opt.flags) & CKPT_OPT_REBUILD_SHARES)
-                return fail(CKPT_EMISMATCH, "protect: members disagree on CKPT_OPT_REBUILD_SHARES (member %u)", j);
+            if ((hb[j]->opt_flags ^ c->opt.flags) & (CKPT_OPT_REBUILD_SHARES | CKPT_OPT_XOR_PUSH))
+                return fail(CKPT_EMISMATCH, "protect: members disagree on CKPT_OPT_REBUILD_SHARES / CKPT_OPT_XOR_PUSH (member %u)", j);
             c->group_version = std::max(c->group_version, hb[j]->attached_id);
         }
         for (uint32_t j = 0; j < m; ++j) {
@@ -636,8 +637,8 @@ extern "C" int ckpt_protect(ckpt_ctx *c, const ckpt_group *g) {
             if (!g->members[j]) return fail(CKPT_EINVAL, "protect: LOCAL group member %u is NULL", j);
             if (g->members[j]->opt.arena_key != c->opt.arena_key)
                 return fail(CKPT_EMISMATCH, "protect: member %u uses another arena key", j);
-            if ((g->members[j]->opt.flags ^ c->opt.flags) & CKPT_OPT_REBUILD_SHARES)
-                return fail(CKPT_EMISMATCH, "protect: members disagree on CKPT_OPT_REBUILD_SHARES (member %u)", j);
+            if ((g->members[j]->opt.flags ^ c->opt.flags) & (CKPT_OPT_REBUILD_SHARES | CKPT_OPT_XOR_PUSH))
+                return fail(CKPT_EMISMATCH, "protect: members disagree on CKPT_OPT_REBUILD_SHARES / CKPT_OPT_XOR_PUSH (member %u)", j);
             c->group_version = std::max(c->group_version, g->members[j]->attached_id);
         }
         for (uint32_t j = 0; j < m; ++j) {

@@ -60,7 +60,7 @@ int load_memops();
 // ------------------------------------------------------------------ constants -------
 namespace reft {
 constexpr uint32_t kMagic = 0x52454654u;  // "REFT"
-constexpr uint32_t kAbiVersion = 1;
+constexpr uint32_t kAbiVersion = 2;  // 2: HandleBlob.opt_flags (CKPT_OPT_REBUILD_SHARES, CKPT_OPT_XOR_PUSH)
 // flag page: 3 arrays of CKPT_MAX_GROUP uint32, each on its own 128-B line
 enum Stage { kReady = 0, kRel = 1, kDone = 2, kNumStages = 3 };
 constexpr uint64_t kFlagStride = 32;  // uint32 per stage line
@@ -137,6 +137,7 @@ struct ckpt_ctx {
     int sm_count = 148;
     int max_ctas = 296;
     int xor_ctas = 296;  // CTA budget of the XOR kernels (CKPT_XOR_CTAS overrides)
+    int xor_ctas_push = 32;  // CTAs of the push-mode encode (CKPT_XOR_CTAS overrides)
     int sticky = CKPT_OK;
     std::string sticky_msg;
 
@@ -354,7 +355,10 @@ int do_encode_range(ckpt_ctx *c, uint64_t k, uint64_t bb, uint64_t be, cudaStrea
 int do_encode(ckpt_ctx *c, uint64_t k, cudaStream_t s);
 int do_rebuild_row(ckpt_ctx *c, uint64_t k, uint32_t kl, cudaStream_t s);
 int do_encode_lost_share(ckpt_ctx *c, uint64_t k, uint32_t kl, cudaStream_t s);
-int rebuild_map_parity(ckpt_ctx *c, uint32_t kl);
+int rebuild_map_parity(ckpt_ctx *c, uint32_t kl, bool wait = false);
+bool xor_push(const ckpt_ctx *c);
+int push_issue(ckpt_ctx *c);
+int push_collect(ckpt_ctx *c);
 // Without CKPT_OPT_REBUILD_SHARES the lost member re-encodes its own parity row (pulling
 // L* more over NVLink); with it the survivors encode it in shares (Q27)
 static inline bool rebuild_self_encode(const ckpt_ctx *c) { return !(c->opt.flags & CKPT_OPT_REBUILD_SHARES); }

@@ -713,6 +713,121 @@ cudaError_t launch_xor_tma_n(const XorArgs &a, int ctas, cudaStream_t s) {
     return cudaGetLastError();
 }
 
+
+// ---------------------------------------------------------------------------------
+// Fabric probe (ckpt_probe_fabric): the load side of xor_tma_kernel alone -- W warps per
+// CTA, lane 0 of each keeps NS 16 KiB cp.async.bulk loads in flight, pieces interleaved
+// over the peers; nothing is stored.
+constexpr int kProbeW = 4, kProbeNS = 3;
+constexpr uint32_t kProbeT = 16384;
+
+__global__ void __launch_bounds__(32 * kProbeW) probe_pull_kernel(const __grid_constant__ ProbeArgs a) {
+    extern __shared__ __align__(128) uint8_t smem[];
+    __shared__ __align__(8) uint64_t bars[kProbeW][kProbeNS];
+    const uint32_t lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    if (lane) return;
+    uint8_t *ring = smem + (size_t)w * kProbeNS * kProbeT;
+    for (int i = 0; i < kProbeNS; ++i) mbar_init(&bars[w][i], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    const uint64_t items = a.n / kProbeT * a.npeers, step = (uint64_t)gridDim.x * kProbeW;
+    const uint64_t first = (uint64_t)blockIdx.x * kProbeW + w;
+    int k = 0;
+    for (uint64_t it = first; it < items && k < kProbeNS; it += step, ++k) {
+        mbar_expect_tx(&bars[w][k], kProbeT);
+        bulk_g2s(ring + (size_t)k * kProbeT, a.src[it % a.npeers] + (it / a.npeers) * kProbeT, kProbeT, &bars[w][k]);
+    }
+    uint32_t phase = 0;
+    int st = 0;
+    for (uint64_t it = first; it < items; it += step) {
+        mbar_wait(&bars[w][st], (phase >> st) & 1);
+        phase ^= 1u << st;
+        const uint64_t nx = it + (uint64_t)kProbeNS * step;
+        if (nx < items) {
+            mbar_expect_tx(&bars[w][st], kProbeT);
+            bulk_g2s(ring + (size_t)st * kProbeT, a.src[nx % a.npeers] + (nx / a.npeers) * kProbeT, kProbeT, &bars[w][st]);
+        }
+        st = st + 1 == kProbeNS ? 0 : st + 1;
+    }
+}
+
+// ---------------------------------------------------------------------------------
+// Push-mode XOR encode (XorPushArgs).  W warps per CTA; lane 0 of each runs a pipeline over
+// tiles of T bytes of the image in order: cp.async.bulk G->S of the tile from local
+// staging (mbarrier), then ONE cp.reduce.async.bulk .xor.b64 S->G into the row owner's
+// parity (over NVLink for a peer), committed as a bulk group; a stage is refilled once the
+// previous tile's reduction has read it (wait_group.read 1), so NS-1 loads and up to two
+// reductions are in flight per warp.  The warp waits for full completion of its reductions
+// before it exits: kernel completion then means every XOR has been performed at the row
+// owners (the REL signal that follows on the stream publishes it).
+constexpr int kPushW = 4, kPushNS = 3;
+constexpr uint32_t kPushT = 16384;
+
+__device__ __forceinline__ void bulk_s2g_xor(void *gmem, const void *smem, uint32_t bytes) {
+    asm volatile("cp.reduce.async.bulk.global.shared::cta.bulk_group.xor.b64 [%0], [%1], %2;" ::"l"(gmem),
+                 "r"(smem_u32(smem)), "r"(bytes)
+                 : "memory");
+}
+
+__global__ void __launch_bounds__(32 * kPushW) xor_push_kernel(const __grid_constant__ XorPushArgs a) {
+    extern __shared__ __align__(128) uint8_t smem[];
+    __shared__ __align__(8) uint64_t bars[kPushW][kPushNS];
+    const uint32_t lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    if (lane) return;
+    uint8_t *ring = smem + (size_t)w * kPushNS * kPushT;
+    for (int i = 0; i < kPushNS; ++i) mbar_init(&bars[w][i], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    const uint64_t u = a.unit, T = u < kPushT ? u : kPushT;
+    const uint64_t tpu = (u + T - 1) / T;
+    const uint64_t rem = a.L % u;
+    // tiles in image order; tile offsets grow monotonically, so those below L are a prefix
+    const uint64_t items = a.L / u * tpu + (rem + T - 1) / T;
+    const uint64_t step = (uint64_t)gridDim.x * kPushW;
+    const uint32_t n1 = a.m - 1;
+    auto geom = [&](uint64_t it, uint64_t &o, uint32_t &len) {
+        const uint64_t q = it / tpu, t = it - q * tpu;
+        o = q * u + t * T;
+        uint64_t l = u - t * T < T ? u - t * T : T;
+        if (o + l > a.L) l = a.L - o;
+        len = (uint32_t)l;
+    };
+    auto load = [&](uint64_t it, int st) {
+        uint64_t o;
+        uint32_t len;
+        geom(it, o, len);
+        mbar_expect_tx(&bars[w][st], len);
+        bulk_g2s(ring + (size_t)st * kPushT, a.src + o, len, &bars[w][st]);
+    };
+    const uint64_t first = (uint64_t)blockIdx.x * kPushW + w;
+    int k = 0;
+    for (uint64_t it = first; it < items && k < kPushNS; it += step, ++k) load(it, k);
+    uint32_t phase = 0;
+    int st = 0, prev_st = 0;
+    uint64_t prev = UINT64_MAX;
+    for (uint64_t it = first; it < items; it += step) {
+        uint64_t o;
+        uint32_t len;
+        geom(it, o, len);
+        const uint64_t q = o / u, s = q / n1;
+        const uint32_t i = (uint32_t)(q - s * n1);
+        const uint32_t r = i < a.me ? i : i + 1;  // sigma(r, me) = i
+        mbar_wait(&bars[w][st], (phase >> st) & 1);
+        phase ^= 1u << st;
+        bulk_s2g_xor(a.dst[r] + s * u + (o - q * u), ring + (size_t)st * kPushT, len);
+        bulk_commit();
+        if (prev != UINT64_MAX) {
+            bulk_wait_read<1>();  // the previous tile's reduction has read its stage
+            const uint64_t nx = prev + (uint64_t)kPushNS * step;
+            if (nx < items) load(nx, prev_st);
+        }
+        prev = it;
+        prev_st = st;
+        st = st + 1 == kPushNS ? 0 : st + 1;
+    }
+    bulk_wait_all();
+}
+
 __global__ void signal_kernel(const SignalArgs a) {
     const int i = threadIdx.x;
     if (i < a.n) asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(a.addr[i]), "r"(a.value) : "memory");
@@ -786,12 +901,37 @@ cudaError_t preload_kernels() {
         (const void *)xor_tma_kernel<1>, (const void *)xor_tma_kernel<2>, (const void *)xor_tma_kernel<3>,
         (const void *)xor_tma_kernel<4>, (const void *)xor_tma_kernel<5>, (const void *)xor_tma_kernel<6>,
         (const void *)xor_tma_kernel<7>, (const void *)xor_tma_kernel<8>,
-        (const void *)signal_kernel};
+        (const void *)signal_kernel, (const void *)probe_pull_kernel, (const void *)xor_push_kernel};
     for (const void *f : fns) {
         cudaError_t e = cudaFuncGetAttributes(&fa, f);
         if (e != cudaSuccess) return e;
     }
     return cudaSuccess;
+}
+
+cudaError_t launch_probe_pull(const ProbeArgs &a, int ctas, cudaStream_t s) {
+    const int smem = kProbeW * kProbeNS * (int)kProbeT;
+    cudaError_t e = cudaFuncSetAttribute(probe_pull_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return e;
+    probe_pull_kernel<<<ctas, 32 * kProbeW, smem, s>>>(a);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_xor_push(const XorPushArgs &a, int ctas, cudaStream_t s) {
+    if (a.m < 2 || a.m > kMaxTerms + 1 || (a.unit & 15) || a.unit == 0 || (a.L & 15) || ((uintptr_t)a.src & 15))
+        return cudaErrorInvalidValue;
+    if (a.L == 0) return cudaSuccess;
+    static unsigned long long attr_set = 0;  // bit d: attribute set on device d
+    const int smem = kPushW * kPushNS * (int)kPushT;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (!(attr_set & (1ull << dev))) {
+        cudaError_t e = cudaFuncSetAttribute(xor_push_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        if (e != cudaSuccess) return e;
+        attr_set |= 1ull << dev;
+    }
+    xor_push_kernel<<<ctas, 32 * kPushW, smem, s>>>(a);
+    return cudaGetLastError();
 }
 
 cudaError_t launch_signal(const SignalArgs &a, cudaStream_t s) {

@@ -92,7 +92,31 @@ struct SignalArgs {
     uint32_t value;
 };
 
+// Push-mode XOR encode (CKPT_OPT_XOR_PUSH): member `me` sends every unit of its own image
+// to the row it belongs to -- unit i of stripe s is term sigma(r, me) = i of row
+// r = i + [i >= me] (Eq 1 P.474-477) -- as a bulk XOR reduction into row owner r's parity
+// stream at P_r[s*u + w] (zeroed by its owner before its pack).  Only image bytes [0, L)
+// are sent; the zero pad contributes nothing (Q5).  Reads are local HBM, writes are posted
+// NVLink reductions (cp.reduce.async.bulk .xor.b64).
+struct XorPushArgs {
+    const uint8_t *src;
+    uint64_t L;
+    uint64_t unit;
+    uint32_t m, me;
+    uint8_t *dst[kMaxTerms + 1];  // parity stream of row owner r (unused for r = me)
+};
+
+// Fabric probe: bulk loads of n bytes from each of the npeers sources (peer staging over
+// NVLink), interleaved over the peers in 16 KiB pieces, data discarded in SMEM.
+struct ProbeArgs {
+    const uint8_t *src[kMaxTerms];
+    int npeers;
+    uint64_t n;
+};
+
 // Launchers (return the cudaError_t of the launch).
+cudaError_t launch_probe_pull(const ProbeArgs &a, int ctas, cudaStream_t s);
+cudaError_t launch_xor_push(const XorPushArgs &a, int ctas, cudaStream_t s);
 cudaError_t launch_signal(const SignalArgs &a, cudaStream_t s);
 cudaError_t preload_kernels();
 cudaError_t launch_pack_all(const PackAllArgs &a, int max_ctas, cudaStream_t s, bool tma);

@@ -249,23 +249,33 @@ int do_encode_lost_share(ckpt_ctx *c, uint64_t k, uint32_t kl, cudaStream_t s) {
 
 // Map lost member kl's parity buffer (survivors only): LOCAL members share the process;
 // IPC members read the handle kl published in its flag page at ckpt_protect.
-int rebuild_map_parity(ckpt_ctx *c, uint32_t kl) {
+int rebuild_map_parity(ckpt_ctx *c, uint32_t kl, bool wait) {
     if (c->me == kl || c->peer_parity[kl]) return CKPT_OK;
     if (c->transport == CKPT_GROUP_LOCAL) {
         c->peer_parity[kl] = c->members[kl]->parity;
         return c->peer_parity[kl] ? CKPT_OK : fail(CKPT_ESTATE, "rebuild: member %u has no parity buffer", kl);
     }
     cudaIpcMemHandle_t h;
-    memset(&h, 0, sizeof h);
+    static const cudaIpcMemHandle_t zero = {};
     cudaStream_t t = nullptr;  // non-blocking: must not wait for the training streams
     CUDA_TRY(cudaStreamCreateWithFlags(&t, cudaStreamNonBlocking));
-    cudaError_t e = cudaMemcpyAsync(&h, (const uint8_t *)c->peer_flags[kl] + kParityHandleOff, sizeof h,
-                                    cudaMemcpyDeviceToHost, t);
-    if (e == cudaSuccess) e = cudaStreamSynchronize(t);
+    // with `wait` (push encode: the peer may still be inside ckpt_protect) poll until the
+    // handle appears, up to CKPT_TIMEOUT_S
+    double limit = 600.0;
+    if (const char *x = getenv("CKPT_TIMEOUT_S")) limit = atof(x);
+    const auto t0 = std::chrono::steady_clock::now();
+    cudaError_t e;
+    for (;;) {
+        memset(&h, 0, sizeof h);
+        e = cudaMemcpyAsync(&h, (const uint8_t *)c->peer_flags[kl] + kParityHandleOff, sizeof h, cudaMemcpyDeviceToHost, t);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(t);
+        if (e != cudaSuccess || !wait || memcmp(&h, &zero, sizeof h)) break;
+        if (std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count() > limit) break;
+        std::this_thread::sleep_for(std::chrono::milliseconds(1));
+    }
     cudaStreamDestroy(t);
     if (e != cudaSuccess) return fail(CKPT_ECUDA, "rebuild: reading member %u's parity handle: %s", kl, cudaGetErrorString(e));
-    static const cudaIpcMemHandle_t zero = {};
-    if (!memcmp(&h, &zero, sizeof h)) return fail(CKPT_EPEER, "rebuild: member %u published no parity handle", kl);
+    if (!memcmp(&h, &zero, sizeof h)) return fail(CKPT_EPEER, "member %u published no parity handle", kl);
     void *p = nullptr;
     e = cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess);
     if (e != cudaSuccess) {
@@ -327,6 +337,9 @@ bool single_launch(const ckpt_ctx *c) {
 int issue_pack_all(ckpt_ctx *c) {
     const uint64_t nb_data = (c->L + c->op_B - 1) / c->op_B;
     int rc;
+    // push encode: the peers XOR-reduce into this parity stream; zero it before anything
+    // this snapshot publishes (the peers' reductions wait for this member's READY)
+    if (xor_push(c)) CUDA_TRY(cudaMemsetAsync(c->parity, 0, c->Lstar / (c->m - 1), c->sP));
     CUDA_TRY(cudaMemsetAsync(c->counters, 0, std::max<uint64_t>(nb_data, 1) * sizeof(uint32_t), c->sP));
     if (c->m >= 2)
         for (uint64_t k = nb_data; k < c->op_NB; ++k)
@@ -477,9 +490,53 @@ bool xor_in_one_launch(const ckpt_ctx *c) {
     return c->m >= 2 && c->aec && single_launch(c) && !(c->opt.flags & CKPT_OPT_CE_GATHER);
 }
 
+bool xor_push(const ckpt_ctx *c) { return (c->opt.flags & CKPT_OPT_XOR_PUSH) && xor_in_one_launch(c); }
+
+// Push-mode encode (CKPT_OPT_XOR_PUSH), part 1 on this member's XOR stream: once this
+// member's pack is done (its own image is the only input) and every peer has zeroed its
+// parity -- which precedes that peer's first READY in its stream order (issue_pack_all) --
+// push every unit of the image into its row owner's parity as bulk XOR reductions, then
+// tell every peer (REL) that its parity holds this member's terms.
+int push_issue(ckpt_ctx *c) {
+    int rc;
+    if (!c->parity_peers_mapped) {  // once: every peer's parity stream, for the reductions
+        for (uint32_t j = 0; j < c->m; ++j)
+            if (j != c->me && (rc = rebuild_map_parity(c, j, true))) return rc;
+        c->parity_peers_mapped = true;
+    }
+    CUDA_TRY(cudaStreamWaitEvent(c->sX, c->ev_pack_all, 0));
+    if ((rc = wait_all(c, c->sX, kReady, bucket_seq(c, 0), slot_of(c, 0)))) return rc;
+    XorPushArgs a;
+    memset(&a, 0, sizeof a);
+    a.src = c->staging;
+    a.L = c->L;
+    a.unit = c->unit;
+    a.m = c->m;
+    a.me = c->me;
+    for (uint32_t r = 0; r < c->m; ++r) a.dst[r] = r == c->me ? nullptr : c->peer_parity[r];
+    TimedLaunch *t;
+    if ((rc = timed_begin(c, c->sX, 1, &t))) return rc;
+    const int ctas = std::max(1, std::min(c->xor_ctas_push, c->max_ctas));
+    CUDA_TRY(launch_xor_push(a, ctas, c->sX));
+    if ((rc = timed_end(t, c->sX))) return rc;
+    c->st.xor_launches++;
+    c->st.xor_bytes_in += c->L;  // NVLink bytes of the encode: this member's image, out
+    c->st.xor_bytes_out += c->Lstar / (c->m - 1);
+    return sig_signal(c, c->sX, kRel, bucket_seq(c, c->op_NB - 1), slot_of(c, c->op_NB - 1));
+}
+
+// Part 2 (after every member's part 1 was issued -- LOCAL groups issue them in one
+// thread): this member's parity row is complete once every peer's REL arrived.
+int push_collect(ckpt_ctx *c) {
+    int rc;
+    if ((rc = wait_all(c, c->sX, kRel, bucket_seq(c, c->op_NB - 1), slot_of(c, c->op_NB - 1)))) return rc;
+    for (uint64_t k = 0; k < c->op_NB; ++k) CUDA_TRY(cudaEventRecord(c->ev_xored[slot_of(c, k)], c->sX));
+    return CKPT_OK;
+}
+
 int stage_xor(ckpt_ctx *c, uint64_t k) {
     if (c->m < 2 || !c->aec) return CKPT_OK;
-    if (xor_in_one_launch(c)) return k + 1 == c->op_NB ? stage_xor_all(c) : CKPT_OK;
+    if (xor_in_one_launch(c)) return k + 1 == c->op_NB ? (xor_push(c) ? push_issue(c) : stage_xor_all(c)) : CKPT_OK;
     const uint32_t s = slot_of(c, k);
     int rc;
     if (c->opt.flags & CKPT_OPT_CE_GATHER) {
@@ -656,6 +713,9 @@ extern "C" int ckpt_snapshot(ckpt_ctx *c, uint64_t bucket_bytes, void *stream, u
                 for (uint32_t j = 0; j < c->m; ++j)
                     if ((rc = set_dev(c->members[j])) || (rc = stage_copy(c->members[j], k, !c->full_copy))) goto bad;
             }
+            if (xor_push(c))
+                for (uint32_t j = 0; j < c->m; ++j)
+                    if ((rc = set_dev(c->members[j])) || (rc = push_collect(c->members[j]))) goto bad;
             for (uint64_t k = 0; c->full_copy && k < c->op_NB; ++k)
                 for (uint32_t j = 0; j < c->m; ++j)
                     if ((rc = set_dev(c->members[j])) || (rc = stage_copy_parity(c->members[j], k))) goto bad;
@@ -685,6 +745,10 @@ extern "C" int ckpt_snapshot(ckpt_ctx *c, uint64_t bucket_bytes, void *stream, u
             make_sticky(c, rc);
             return rc;
         }
+    }
+    if (xor_push(c) && (rc = push_collect(c))) {
+        make_sticky(c, rc);
+        return rc;
     }
     for (uint64_t k = 0; c->full_copy && k < c->op_NB; ++k) {
         if ((rc = stage_copy_parity(c, k))) {
@@ -814,7 +878,7 @@ extern "C" int ckpt_wait(ckpt_ctx *c, uint64_t id) {
     if (c->transport == CKPT_GROUP_IPC && c->aec && c->m >= 2 && !c->parity_peers_mapped && !rebuild_self_encode(c)) {
         c->parity_peers_mapped = true;
         for (uint32_t j = 0; j < c->m; ++j)
-            if (j != c->me && rebuild_map_parity(c, j)) cudaGetLastError();
+            if (j != c->me && rebuild_map_parity(c, j, false)) cudaGetLastError();
     }
     return CKPT_OK;
 }

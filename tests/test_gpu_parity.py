@@ -133,6 +133,46 @@ def test_rebuild_shares_flag_must_agree(torch, C):
             C.ckpt_destroy(c)
 
 
+@pytest.mark.parametrize("m,unit", [(2, 65536), (3, 4096), (4, 16), (8, 0)])
+def test_push_encode_repeated_snapshots(torch, C, m, unit):
+    """CKPT_OPT_XOR_PUSH: every row owner zeroes its parity before each snapshot and its
+    peers XOR-reduce their units into it (Eq 1); three snapshots of changing state (the
+    second would read P xor P = 0 if the zeroing were missing) each equal the oracle."""
+    from synth.gpu import fill_state
+    states, ctxs = make_group(torch, C, m, unit, 0, 1 << 16, flags=C.CKPT_OPT_XOR_PUSH, misalign=1)
+    try:
+        for step in range(3):
+            if step:
+                for j, (specs, ts) in enumerate(states):
+                    fill_state(ts, j, seed=synth.SEED + step)  # a later training step
+            snapshot_group(C, ctxs)
+            g = C.ckpt_geometry(ctxs[0])
+            Ds = [oracle_image(specs, j, g["L_star"], seed=synth.SEED + step)[0] for j, (specs, _) in enumerate(states)]
+            Ps = oracle.encode_all(Ds, g["unit"])
+            for j, c in enumerate(ctxs):
+                d, p = C.ckpt_host_view(c, 0, copy=True)
+                assert_bytes_equal(d, Ds[j], f"step {step} rank {j} data")
+                assert_bytes_equal(p, Ps[j], f"step {step} rank {j} parity")
+    finally:
+        for c in ctxs:
+            C.ckpt_destroy(c)
+
+
+def test_xor_push_flag_must_agree(torch, C):
+    """Push and pull encodes write a parity row differently (reductions from the peers vs a
+    store by its owner): a group that mixes them is refused."""
+    states = [tiny(j) for j in range(3)]
+    ctxs = [make_ctx(C, st, n_slots=0, bucket_bytes=1 << 20, flags=C.CKPT_OPT_XOR_PUSH if j == 2 else 0)
+            for j, st in enumerate(states)]
+    try:
+        with pytest.raises(C.CkptError) as e:
+            C.protect_local(ctxs)
+        assert e.value.code == C.CKPT_EMISMATCH
+    finally:
+        for c in ctxs:
+            C.ckpt_destroy(c)
+
+
 def snapshot_group(C, ctxs, bucket=0):
     ids = [C.ckpt_snapshot(c, bucket) for c in ctxs]
     for c, i in zip(ctxs, ids):
@@ -148,7 +188,7 @@ def expected_group(states, Lstar, unit):
 @pytest.mark.parametrize("m", [2, 3, 4, 8])
 @pytest.mark.parametrize("unit,n_slots,bucket", [(65536, 0, 1 << 20), (4096, 3, 1 << 20), (16, 2, 4096),
                                                  (0, 0, 1 << 20), (65536, 4, 1 << 20)])
-@pytest.mark.parametrize("flags", [0, 0x4, 0x10, 0x18])
+@pytest.mark.parametrize("flags", [0, 0x4, 0x10, 0x18, 0x400])
 def test_group_encode_matches_oracle(torch, C, m, unit, n_slots, bucket, flags):
     if unit == 65536 and n_slots and (m - 1) * unit > bucket:
         pytest.skip("stripe larger than ring slot")
@@ -174,7 +214,10 @@ def test_group_encode_matches_oracle(torch, C, m, unit, n_slots, bucket, flags):
                                                   (4, 65536, 0, 0x80), (3, 4096, 0, 0x82), (5, 4096, 0, 0x88),
                                                   # CKPT_OPT_REBUILD_SHARES (Q27): survivors encode the lost row
                                                   (2, 4096, 0, 0x200), (4, 4096, 2, 0x200), (5, 65536, 0, 0x202),
-                                                  (8, 1024, 3, 0x200), (3, 4096, 0, 0x280), (7, 16, 0, 0x200)])
+                                                  (8, 1024, 3, 0x200), (3, 4096, 0, 0x280), (7, 16, 0, 0x200),
+                                                  # CKPT_OPT_XOR_PUSH: push-mode encode (bulk XOR reductions)
+                                                  (2, 4096, 0, 0x400), (4, 65536, 0, 0x402), (8, 1024, 0, 0x600),
+                                                  (5, 16, 0, 0x480)])
 def test_group_drill_rebuild_every_rank(torch, C, m, unit, n_slots, flags):
     """Failure drill (Q12): rank k loses tensors and host image; rebuild + load."""
     from synth.gpu import fill_state
@@ -335,8 +378,8 @@ def test_c2_bench_config_full_image(torch, C):
         C.ckpt_destroy(ctx)
 
 
-@pytest.mark.parametrize("m,k", [(2, 1), (3, 0), (4, 2)])
-def test_c2_group_full_image_and_rebuild(torch, C, m, k):
+@pytest.mark.parametrize("m,k,push", [(2, 1, 0), (3, 0, 0), (4, 2, 0), (4, 1, 1)])
+def test_c2_group_full_image_and_rebuild(torch, C, m, k, push):
     """BASELINE config 2 at full size as an m-member protection group on one device
     (CKPT_GROUP_LOCAL: the same pack_all_tma_kernel and xor_tma_kernel<m-1> launches as the
     one-process-per-GPU product, full-copy staging, 512 MiB buckets, one host buffer).
@@ -355,7 +398,9 @@ def test_c2_group_full_image_and_rebuild(torch, C, m, k):
         for j in range(m):
             specs, ts = make_rank_state("c2_7b_tp8", j, "cuda:0")
             states.append((specs, ts))
-            ctx = C.ckpt_create(0, bench_options(C, host_buffers=1))
+            o = bench_options(C, host_buffers=1)
+            o.flags |= C.CKPT_OPT_XOR_PUSH if push else 0
+            ctx = C.ckpt_create(0, o)
             ctxs.append(ctx)
             C.ckpt_register(ctx, descriptors(ts, specs))
         C.protect_local(ctxs)

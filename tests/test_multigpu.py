@@ -137,6 +137,8 @@ def _world():
     ("tiny_5", 256, 0, 1 << 20, 0x10, 0),
     ("tiny_7", 4096, 0, 1 << 20, 0x200, 1),  # CKPT_OPT_REBUILD_SHARES (Q27)
     ("tiny_5", 1024, 2, 1 << 16, 0x200, 0),
+    ("tiny_7", 4096, 0, 1 << 20, 0x400, 1),  # CKPT_OPT_XOR_PUSH: bulk XOR reductions over NVLink
+    ("tiny_6", 16, 0, 1 << 16, 0x600, 0),
 ])
 def test_ipc_group_all_gpus(case):
     _run(min(_world(), 8), case)
@@ -151,7 +153,7 @@ def test_ipc_c1_16mib_all_gpus():
     _run(min(_world(), 8), ("c1_16mb_fp32_m8", 65536, 0, 64 << 20, 0, 0))
 
 
-def _worker_c2(rank, world, port, q, config="c2_7b_tp8"):
+def _worker_c2(rank, world, port, q, config="c2_7b_tp8", extra_flags=0):
     try:
         os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank), WORLD_SIZE=str(world))
         import torch
@@ -169,7 +171,7 @@ def _worker_c2(rank, world, port, q, config="c2_7b_tp8"):
         # bench.py's launch configuration: full-copy staging, 512 MiB buckets, TMA pack
         ctx = C.ckpt_create(rank, C.ckpt_options_default(
             n_slots=0, bucket_bytes=512 << 20, stripe_unit=64 << 10,
-            flags=C.CKPT_OPT_TIMING | C.CKPT_OPT_HOST_LOAD | C.CKPT_OPT_TMA_PACK, host_buffers=1))
+            flags=C.CKPT_OPT_TIMING | C.CKPT_OPT_HOST_LOAD | C.CKPT_OPT_TMA_PACK | extra_flags, host_buffers=1))
         C.ckpt_register(ctx, descriptors(ts, specs))
         C.protect_ipc(ctx)
         g = C.ckpt_geometry(ctx)
@@ -214,8 +216,8 @@ def _worker_c2(rank, world, port, q, config="c2_7b_tp8"):
         q.put((rank, None, traceback.format_exc(), None))
 
 
-@pytest.mark.parametrize("config", ["c2_7b_tp8", "c4_34b_tp8_stage0"])
-def test_ipc_full_size_full_image(config):
+@pytest.mark.parametrize("config,flags", [("c2_7b_tp8", 0), ("c4_34b_tp8_stage0", 0), ("c2_7b_tp8", 0x400)])
+def test_ipc_full_size_full_image(config, flags):
     """BASELINE configs 2 and 4 at full size in the bench launch configuration (one
     process per GPU, full-copy staging, 512 MiB buckets, TMA pack, TMA XOR over NVLink).
     Unsampled: every byte of every rank's data (O3) and parity row (O4, Eq 1 P.474-477)
@@ -229,7 +231,7 @@ def test_ipc_full_size_full_image(config):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    ps = [ctx.Process(target=_worker_c2, args=(r, world, port, q, config)) for r in range(world)]
+    ps = [ctx.Process(target=_worker_c2, args=(r, world, port, q, config, flags)) for r in range(world)]
     for p in ps:
         p.start()
     res, t0 = [], time.time()
