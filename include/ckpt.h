@@ -268,6 +268,11 @@ int ckpt_fence(ckpt_ctx *ctx, uint64_t id, void *stream);
  * Errors: ECUDA (sticky async error; commit refused), ESTATE (no such snapshot). */
 int ckpt_wait(ckpt_ctx *ctx, uint64_t id);
 
+/* Non-blocking: *done = 1 when snapshot `id` has landed everywhere ckpt_wait waits for
+ * (ckpt_wait then returns at once and commits), else 0.  Never commits by itself.
+ * Errors: EINVAL, ESTATE (unknown id), ECUDA. */
+int ckpt_test(ckpt_ctx *ctx, uint64_t id, int *done);
+
 /* Restore every registered tensor from the last COMPLETED image (H2D + unpack),
  * ordered on `stream`; returns after enqueueing (stream-ordered, host-async).
  * Local only: no communication.  With full-copy staging the library's device copy of
@@ -364,6 +369,10 @@ int ckpt_arena_unlink(uint64_t key, uint32_t m, uint32_t nbuf);
  * never reopened does not complete (ckpt_wait times out). */
 #define CKPT_WINDOW_BUBBLE  0x1u
 #define CKPT_WINDOW_COMPUTE 0x2u
+#define CKPT_WINDOW_COMM    0x4u  /* Layer 3 (P.425): a communication phase of training on
+                                     another interconnect than the snapshot's (NVLink
+                                     collectives while the D2H uses PCIe); used only by the
+                                     buckets ckpt_has_apply_layers assigns to it            */
 int ckpt_window(ckpt_ctx *ctx, int open, void *stream);
 
 /* Alg 1 SplitParameter into the scheduler (lines 10-12): image bytes [0, bubble_bytes),
@@ -373,6 +382,14 @@ int ckpt_window(ckpt_ctx *ctx, int open, void *stream);
  * UINT64_MAX (the default) = all in bubbles.  Takes effect at the next snapshot.
  * Errors: EINVAL. */
 int ckpt_has_apply(ckpt_ctx *ctx, uint64_t bubble_bytes);
+
+/* The three layers of HAS (P.419-425) in the scheduler: image bytes [0, bubble_bytes) go
+ * out only in bubbles (Layer 1), [bubble_bytes, bubble_bytes + compute_bytes) in bubble or
+ * compute windows (Layer 2), the rest in bubble, compute or communication windows (Layer 3:
+ * "not used unless the previous layers are not enough").  Whole buckets, rounded up at each
+ * snapshot.  ckpt_has_apply(ctx, b) is ckpt_has_apply_layers(ctx, b, UINT64_MAX).
+ * Errors: EINVAL. */
+int ckpt_has_apply_layers(ckpt_ctx *ctx, uint64_t bubble_bytes, uint64_t compute_bytes);
 
 /* Alg 1's estimators, host-only.  EstimateSnapshotTime = bytes / B_io; EstimateBubbleTime
  * = (0.8 p + 2|P| - p - 2) * C_FB,BP (1F1B, stage p of |P|, clamped at 0); SplitParameter:
@@ -385,6 +402,20 @@ typedef struct ckpt_has_plan_t {
 } ckpt_has_plan_t;
 int ckpt_has_plan(uint32_t stage, uint32_t num_stages, double c_fb_bp_s, uint64_t snapshot_bytes,
                   double b_io_bytes_per_s, ckpt_has_plan_t *out);
+
+/* Alg 1 extended to Layers 2 and 3 (reading Q28): the bubble part is ckpt_has_plan's
+ * W_bubble exactly; of the rest W_*, the first floor(n * t_compute / t_ss) bytes (at most
+ * W_*) go alongside computation -- t_compute_s is the computation time per iteration in
+ * which the caller opens compute windows -- and whatever is left goes to Layer 3.
+ * Host-only.  Errors: EINVAL (as ckpt_has_plan, or t_compute_s < 0). */
+typedef struct ckpt_has_plan3_t {
+    double t_ss, t_bubble, t_compute;  /* seconds                                           */
+    uint64_t bubble_bytes;             /* Layer 1 (= ckpt_has_plan's W_bubble)              */
+    uint64_t compute_bytes;            /* Layer 2                                           */
+    uint64_t comm_bytes;               /* Layer 3                                           */
+} ckpt_has_plan3_t;
+int ckpt_has_plan3(uint32_t stage, uint32_t num_stages, double c_fb_bp_s, uint64_t snapshot_bytes,
+                   double b_io_bytes_per_s, double t_compute_s, ckpt_has_plan3_t *out);
 
 /* ---- fabric probe (measurement; "NVLink ... to be measured P2P, all
  * ranks concurrent") --------------------------------------------------------------------

@@ -93,6 +93,11 @@ class ckpt_has_plan_t(ctypes.Structure):
                 ("compute_bytes", _u64)]
 
 
+class ckpt_has_plan3_t(ctypes.Structure):
+    _fields_ = [("t_ss", ctypes.c_double), ("t_bubble", ctypes.c_double), ("t_compute", ctypes.c_double),
+                ("bubble_bytes", _u64), ("compute_bytes", _u64), ("comm_bytes", _u64)]
+
+
 CKPT_AOR_PERSIST = 0x1
 CKPT_AOR_EMPTY, CKPT_AOR_CLEAN, CKPT_AOR_UPDATING, CKPT_AOR_POISONED, CKPT_AOR_SEEDING = 0, 1, 2, 3, 4
 
@@ -141,12 +146,16 @@ def lib():
             "ckpt_snapshot": (ctypes.c_int, [_vp, _u64, _vp, ctypes.POINTER(_u64)]),
             "ckpt_fence": (ctypes.c_int, [_vp, _u64, _vp]),
             "ckpt_wait": (ctypes.c_int, [_vp, _u64]),
+            "ckpt_test": (ctypes.c_int, [_vp, _u64, ctypes.POINTER(ctypes.c_int)]),
             "ckpt_load": (ctypes.c_int, [_vp, _vp]),
             "ckpt_rebuild": (ctypes.c_int, [_vp, _i32, _vp]),
             "ckpt_recover": (ctypes.c_int, [_vp, _u32, _vp]),
             "ckpt_sync": (ctypes.c_int, [_vp]),
             "ckpt_window": (ctypes.c_int, [_vp, ctypes.c_int, _vp]),
             "ckpt_has_apply": (ctypes.c_int, [_vp, _u64]),
+            "ckpt_has_apply_layers": (ctypes.c_int, [_vp, _u64, _u64]),
+            "ckpt_has_plan3": (ctypes.c_int, [_u32, _u32, ctypes.c_double, _u64, ctypes.c_double, ctypes.c_double,
+                                              ctypes.POINTER(ckpt_has_plan3_t)]),
             "ckpt_has_plan": (ctypes.c_int, [_u32, _u32, ctypes.c_double, _u64, ctypes.c_double,
                                              ctypes.POINTER(ckpt_has_plan_t)]),
             "ckpt_forget": (ctypes.c_int, [_vp, ctypes.c_uint8]),
@@ -309,6 +318,12 @@ def ckpt_wait(ctx: int, sid: int) -> None:
     _check(lib().ckpt_wait(ctx, sid), "ckpt_wait")
 
 
+def ckpt_test(ctx: int, sid: int) -> bool:
+    d = ctypes.c_int()
+    _check(lib().ckpt_test(ctx, sid, ctypes.byref(d)), "ckpt_test")
+    return bool(d.value)
+
+
 def ckpt_load(ctx: int, stream=None) -> None:
     _check(lib().ckpt_load(ctx, _stream_handle(stream)), "ckpt_load")
 
@@ -321,7 +336,7 @@ def ckpt_recover(ctx: int, lost_mask: int, stream=None) -> None:
     _check(lib().ckpt_recover(ctx, lost_mask, _stream_handle(stream)), "ckpt_recover")
 
 
-CKPT_WINDOW_BUBBLE, CKPT_WINDOW_COMPUTE = 0x1, 0x2
+CKPT_WINDOW_BUBBLE, CKPT_WINDOW_COMPUTE, CKPT_WINDOW_COMM = 0x1, 0x2, 0x4
 
 
 def ckpt_window(ctx: int, open_, stream=None) -> None:
@@ -335,6 +350,20 @@ def ckpt_window(ctx: int, open_, stream=None) -> None:
 
 def ckpt_has_apply(ctx: int, bubble_bytes: int) -> None:
     _check(lib().ckpt_has_apply(ctx, bubble_bytes), "ckpt_has_apply")
+
+
+def ckpt_has_apply_layers(ctx: int, bubble_bytes: int, compute_bytes: int) -> None:
+    _check(lib().ckpt_has_apply_layers(ctx, bubble_bytes, compute_bytes), "ckpt_has_apply_layers")
+
+
+def ckpt_has_plan3(stage: int, num_stages: int, c_fb_bp_s: float, snapshot_bytes: int, b_io: float,
+                   t_compute_s: float) -> dict:
+    """Alg 1 extended to HAS Layers 2 and 3 (host-only; reading Q28)."""
+    o = ckpt_has_plan3_t()
+    _check(lib().ckpt_has_plan3(stage, num_stages, c_fb_bp_s, snapshot_bytes, b_io, t_compute_s, ctypes.byref(o)),
+           "ckpt_has_plan3")
+    return {"t_ss": o.t_ss, "t_bubble": o.t_bubble, "t_compute": o.t_compute, "bubble_bytes": o.bubble_bytes,
+            "compute_bytes": o.compute_bytes, "comm_bytes": o.comm_bytes}
 
 
 def ckpt_has_plan(stage: int, num_stages: int, c_fb_bp_s: float, snapshot_bytes: int, b_io: float) -> dict:

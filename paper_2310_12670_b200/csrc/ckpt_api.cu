@@ -724,8 +724,8 @@ extern "C" int ckpt_window(ckpt_ctx *c, int open, void *stream) {
     if (load_memops()) return fail(CKPT_ECUDA, "window: stream memory operations unavailable");
     int rc = set_dev(c);
     if (rc) return rc;
-    if (open < 0 || (open & ~(int)(CKPT_WINDOW_BUBBLE | CKPT_WINDOW_COMPUTE)))
-        return fail(CKPT_EINVAL, "window: open must be a mask of CKPT_WINDOW_BUBBLE | CKPT_WINDOW_COMPUTE");
+    if (open < 0 || (open & ~(int)(CKPT_WINDOW_BUBBLE | CKPT_WINDOW_COMPUTE | CKPT_WINDOW_COMM)))
+        return fail(CKPT_EINVAL, "window: open must be a mask of CKPT_WINDOW_BUBBLE | CKPT_WINDOW_COMPUTE | CKPT_WINDOW_COMM");
     CUresult r = p_write32((CUstream)stream, (CUdeviceptr)(uintptr_t)c->window, (uint32_t)open,
                            CU_STREAM_WRITE_VALUE_DEFAULT);
     if (r != CUDA_SUCCESS) return fail(CKPT_ECUDA, "cuStreamWriteValue32(window) failed (%d)", (int)r);
@@ -733,8 +733,30 @@ extern "C" int ckpt_window(ckpt_ctx *c, int open, void *stream) {
 }
 
 extern "C" int ckpt_has_apply(ckpt_ctx *c, uint64_t bubble_bytes) {
+    return ckpt_has_apply_layers(c, bubble_bytes, UINT64_MAX);
+}
+
+extern "C" int ckpt_has_apply_layers(ckpt_ctx *c, uint64_t bubble_bytes, uint64_t compute_bytes) {
     if (!c) return fail(CKPT_EINVAL, "has_apply: null");
     c->has_bubble_bytes = bubble_bytes;
+    c->has_compute_bytes = compute_bytes;
+    return CKPT_OK;
+}
+
+extern "C" int ckpt_has_plan3(uint32_t p, uint32_t P, double c, uint64_t bytes, double bio, double t_compute,
+                              ckpt_has_plan3_t *out) {
+    if (!out || t_compute < 0) return fail(CKPT_EINVAL, "has_plan3: bad args");
+    ckpt_has_plan_t a;
+    int rc = ckpt_has_plan(p, P, c, bytes, bio, &a);
+    if (rc) return rc;
+    out->t_ss = a.t_ss;
+    out->t_bubble = a.t_bubble;
+    out->t_compute = t_compute;
+    out->bubble_bytes = a.bubble_bytes;
+    const uint64_t rest = a.compute_bytes;
+    const double cap = a.t_ss > 0 ? std::floor((double)bytes * t_compute / a.t_ss) : (double)rest;
+    out->compute_bytes = cap >= (double)rest ? rest : (uint64_t)cap;
+    out->comm_bytes = rest - out->compute_bytes;
     return CKPT_OK;
 }
 

@@ -161,6 +161,7 @@ struct ckpt_ctx {
     uint32_t *counters = nullptr;  // per-bucket CTA completion counters (single-launch pack)
     uint32_t *window = nullptr;    // HAS window word (device, CKPT_WINDOW_* mask), written by memops
     uint64_t has_bubble_bytes = UINT64_MAX;  // Alg 1 split: image bytes snapshotted in bubbles
+    uint64_t has_compute_bytes = UINT64_MAX; // Layer 2 share after them; the rest is Layer 3
 
     // group
     bool grouped = false;  // ckpt_protect succeeded (m >= 2) or m == 1 arena set up
@@ -282,12 +283,17 @@ static inline uint8_t *parity_slot_ptr_at(const ckpt_ctx *c, uint8_t *parity, ui
 
 static inline uint8_t *parity_slot_ptr(const ckpt_ctx *c, uint64_t k) { return parity_slot_ptr_at(c, c->parity, k); }
 
-// Alg 1 placement of bucket k (ckpt_has_apply): the buckets that start below the split
-// go out only in bubbles; the others alongside computation -- or in a bubble, which is
-// never worse (reading Q26).  The wait passes when (window & mask) != 0.
+// Alg 1 placement of bucket k (ckpt_has_apply_layers): the buckets that start below the
+// split go out only in bubbles; the next compute_bytes alongside computation -- or in a
+// bubble, which is never worse (reading Q26); the rest also in communication windows
+// (Layer 3, reading Q28).  The wait passes when (window & mask) != 0.
 static inline uint32_t window_of(const ckpt_ctx *c, uint64_t k) {
-    return bucket_begin(c, k) < c->has_bubble_bytes ? CKPT_WINDOW_BUBBLE
-                                                    : (CKPT_WINDOW_BUBBLE | CKPT_WINDOW_COMPUTE);
+    const uint64_t b = bucket_begin(c, k);
+    if (b < c->has_bubble_bytes) return CKPT_WINDOW_BUBBLE;
+    const uint64_t l2 = c->has_compute_bytes > UINT64_MAX - c->has_bubble_bytes ? UINT64_MAX
+                                                                               : c->has_bubble_bytes + c->has_compute_bytes;
+    return b < l2 ? (CKPT_WINDOW_BUBBLE | CKPT_WINDOW_COMPUTE)
+                  : (CKPT_WINDOW_BUBBLE | CKPT_WINDOW_COMPUTE | CKPT_WINDOW_COMM);  // Layer 3 (P.425)
 }
 
 static inline uint32_t bucket_seq(const ckpt_ctx *c, uint64_t k) { return c->op_seq_base + (uint32_t)k + 1; }
@@ -345,7 +351,6 @@ void meta_commit(ckpt_ctx *c);
 int ensure_holder_mapped(ckpt_ctx *c);
 int ensure_next_mapped(ckpt_ctx *c);
 int setup_ungrouped(ckpt_ctx *c);
-bool signal_by_kernel();
 int sig_signal(ckpt_ctx *c, cudaStream_t s, int stage, uint32_t seq, uint32_t slot);
 int sig_wait(ckpt_ctx *c, cudaStream_t s, uint32_t j, int stage, uint32_t seq, uint32_t slot);
 int wait_all(ckpt_ctx *c, cudaStream_t s, int stage, uint32_t seq, uint32_t slot, int32_t skip = -1);

@@ -84,13 +84,6 @@ struct PackAllArgs {
     int unpack;            // 1: the load direction (image -> tensors), nothing is published
 };
 
-// Cross-rank signal by a one-warp kernel: st.release.sys of `value` to every address
-// (peers' IPC-mapped flag words).  Alternative to cuStreamWriteValue32 (CKPT_SIGNAL=kernel).
-struct SignalArgs {
-    uint32_t *addr[kMaxTerms];
-    int n;
-    uint32_t value;
-};
 
 // Push-mode XOR encode (CKPT_OPT_XOR_PUSH): member `me` sends every unit of its own image
 // to the row it belongs to -- unit i of stripe s is term sigma(r, me) = i of row
@@ -117,7 +110,6 @@ struct ProbeArgs {
 // Launchers (return the cudaError_t of the launch).
 cudaError_t launch_probe_pull(const ProbeArgs &a, int ctas, cudaStream_t s);
 cudaError_t launch_xor_push(const XorPushArgs &a, int ctas, cudaStream_t s);
-cudaError_t launch_signal(const SignalArgs &a, cudaStream_t s);
 cudaError_t preload_kernels();
 cudaError_t launch_pack_all(const PackAllArgs &a, int max_ctas, cudaStream_t s, bool tma);
 cudaError_t launch_pack(const PackArgs &a, int max_ctas, cudaStream_t s, bool tma);

@@ -5,18 +5,8 @@ using namespace reft;
 
 
 // ------------------------------------------------------------------ signals ---------
-// IPC signals: cuStreamWriteValue32 into the peer's flag page (default, zero SMs) or a
-// one-warp st.release.sys kernel (CKPT_SIGNAL=kernel).  Waits are always
+// IPC signals: cuStreamWriteValue32 into the peer's flag page (zero SMs).  Waits are
 // cuStreamWaitValue32 on the local flag page.
-bool signal_by_kernel() {
-    static int v = -1;
-    if (v < 0) {
-        const char *e = getenv("CKPT_SIGNAL");
-        v = (e && strcmp(e, "kernel") == 0) ? 1 : 0;
-    }
-    return v == 1;
-}
-
 // signal(stage, seq): tell every other member that this member reached `seq`.
 int sig_signal(ckpt_ctx *c, cudaStream_t s, int stage, uint32_t seq, uint32_t slot) {
     if (c->m < 2) return CKPT_OK;
@@ -25,15 +15,6 @@ int sig_signal(ckpt_ctx *c, cudaStream_t s, int stage, uint32_t seq, uint32_t sl
             return stage == kReady ? ready_row(c->peer_flags[j], c->me) + seq % kMaxB
                                    : c->peer_flags[j] + stage * kFlagStride + c->me;
         };
-        if (signal_by_kernel()) {
-            SignalArgs a;
-            memset(&a, 0, sizeof a);
-            for (uint32_t j = 0; j < c->m; ++j)
-                if (j != c->me) a.addr[a.n++] = addr(j);
-            a.value = seq;
-            CUDA_TRY(launch_signal(a, s));
-            return CKPT_OK;
-        }
         for (uint32_t j = 0; j < c->m; ++j) {
             if (j == c->me) continue;
             CUdeviceptr a = (CUdeviceptr)(uintptr_t)addr(j);
@@ -637,8 +618,7 @@ int stage_finish(ckpt_ctx *c) {
     const uint32_t done_seq = c->op_seq_base + (uint32_t)c->op_NB + 1;
     int rc;
     if (c->m >= 2 && (rc = sig_signal(c, c->sC, kDone, done_seq, 0))) return rc;
-    static const bool legacy = getenv("CKPT_WAIT_LEGACY") != nullptr;  // A/B knob
-    if (!legacy && (c->m < 2 || c->transport == CKPT_GROUP_IPC)) {
+    if (c->m < 2 || c->transport == CKPT_GROUP_IPC) {
         // completion = this member's last stream event and every peer's DONE, all queued on
         // sW now: ckpt_wait then polls ONE stream (small snapshots are latency-bound)
         CUDA_TRY(cudaStreamWaitEvent(c->sW, c->ev_done, 0));
@@ -809,8 +789,7 @@ int sync_stream_timeout(ckpt_ctx *c, cudaStream_t s, const char *what) {
             cudaGetLastError();
             return fail(CKPT_EPEER, "%s: timed out after %.0f s waiting for peers (member %u: %s)", what, limit, c->me, buf);
         }
-        static const bool legacy = getenv("CKPT_WAIT_LEGACY") != nullptr;
-        if (el < 0.002 && !legacy) {  // the first 2 ms: poll without sleeping (small snapshots)
+        if (el < 0.002) {  // the first 2 ms: poll without sleeping (small snapshots)
             std::this_thread::yield();
             continue;
         }
@@ -839,6 +818,37 @@ int wait_done_all(ckpt_ctx *c, uint32_t done_seq) {
             }
         }
     }
+    return CKPT_OK;
+}
+
+// Non-blocking completion test: *done = 1 once ckpt_wait(id) would return without waiting.
+extern "C" int ckpt_test(ckpt_ctx *c, uint64_t id, int *done) {
+    if (!c || !done) return fail(CKPT_EINVAL, "test: null");
+    if (id == 0 || id >= c->next_id) return fail(CKPT_ESTATE, "test: unknown snapshot id %llu", (unsigned long long)id);
+    *done = 0;
+    if (id != c->pending_id) {
+        *done = c->completed_id >= id ? 1 : 0;
+        return CKPT_OK;
+    }
+    if (!c->issued) return CKPT_OK;
+    int rc = set_dev(c);
+    if (rc) return rc;
+    auto ready = [](cudaError_t e) { return e == cudaSuccess ? 1 : e == cudaErrorNotReady ? 0 : -1; };
+    int r = 1;
+    if (c->done_enqueued) {
+        r = ready(cudaStreamQuery(c->sW));
+    } else {
+        cudaStream_t ss[4] = {c->sP, c->sX, c->sC, c->sG};
+        for (auto x : ss)
+            if (r == 1) r = ready(cudaStreamQuery(x));
+        for (uint32_t j = 0; r == 1 && c->m >= 2 && c->transport == CKPT_GROUP_LOCAL && j < c->m; ++j)
+            r = ready(cudaEventQuery(c->members[j]->ev_done));
+    }
+    if (r < 0) {
+        cudaError_t e = cudaGetLastError();
+        return fail(CKPT_ECUDA, "test: %s", cudaGetErrorString(e));
+    }
+    *done = r;
     return CKPT_OK;
 }
 

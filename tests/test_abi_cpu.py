@@ -114,6 +114,28 @@ def test_has_plan_spec_vectors(C):
         C.ckpt_has_plan(4, 4, 1.0, 1, 1.0)
 
 
+def test_has_plan3_layers(C):
+    """HAS Layers 1-3 (P.419-425, reading Q28): Layer 1 is Alg 1's W_bubble unchanged; Layer 2
+    takes floor(n * t_compute / t_ss) of the rest; Layer 3 only what the first two cannot
+    hold ("not used unless the previous layers are not enough"); the three partition n."""
+    # n = 100, t_ss = 10, t_bubble = 4 (p=0, |P|=3, C=1): W_bubble = 40 as in Alg 1
+    p = C.ckpt_has_plan3(0, 3, 1.0, 100, 10.0, 3.0)   # compute holds 30 of the remaining 60
+    assert (p["bubble_bytes"], p["compute_bytes"], p["comm_bytes"]) == (40, 30, 30)
+    p = C.ckpt_has_plan3(0, 3, 1.0, 100, 10.0, 6.0)   # compute holds all 60: no Layer 3
+    assert (p["bubble_bytes"], p["compute_bytes"], p["comm_bytes"]) == (40, 60, 0)
+    p = C.ckpt_has_plan3(0, 3, 1.0, 100, 10.0, 0.0)   # no compute window: the rest is Layer 3
+    assert (p["bubble_bytes"], p["compute_bytes"], p["comm_bytes"]) == (40, 0, 60)
+    p = C.ckpt_has_plan3(0, 6, 1.0, 100, 20.0, 0.0)   # bubbles hold everything
+    assert (p["bubble_bytes"], p["compute_bytes"], p["comm_bytes"]) == (100, 0, 0)
+    for args in [(0, 4, 0.7, 12345, 3.0, 1.1), (2, 4, 0.3, 10 ** 9, 7.0, 0.05), (0, 1, 1.0, 999, 1.0, 0.5)]:
+        p = C.ckpt_has_plan3(*args)
+        q = C.ckpt_has_plan(*args[:5])
+        assert p["bubble_bytes"] == q["bubble_bytes"]
+        assert p["bubble_bytes"] + p["compute_bytes"] + p["comm_bytes"] == args[3]
+    with pytest.raises(C.CkptError):
+        C.ckpt_has_plan3(0, 3, 1.0, 100, 10.0, -1.0)
+
+
 # ---------------------------------------------------------------- AOR host arithmetic ----
 @pytest.mark.parametrize("bf16", [False, True])
 def test_aor_host_update_matches_oracle(C, bf16):

@@ -755,7 +755,48 @@ def test_has_split_places_buckets_in_their_windows(torch, C):
         C.ckpt_wait(ctx, sid)
         assert_bytes_equal(C.ckpt_host_view(ctx, 0, copy=True)[0], want, "image after a compute window")
         with pytest.raises(C.CkptError):
-            C.ckpt_window(ctx, 4, s)
+            C.ckpt_window(ctx, 8, s)
+    finally:
+        C.ckpt_destroy(ctx)
+
+
+def test_has_three_layers_place_buckets(torch, C):
+    """HAS Layers 1-3 (P.419-425) in the scheduler (ckpt_has_apply_layers): bubble buckets
+    move only in bubbles, the next compute_bytes in compute (or bubble) windows, the rest
+    also in communication windows (Layer 3, reading Q28); a communication window alone moves
+    only Layer-3 buckets, so the image stays incomplete until the other windows open; the
+    committed image matches the oracle."""
+    import time
+    st = tiny(0, n=9)
+    specs, ts = st
+    B = 1 << 16
+    ctx = make_ctx(C, st, n_slots=0, bucket_bytes=B, flags=C.CKPT_OPT_WINDOWED)
+    s = torch.cuda.Stream()
+    try:
+        C.ckpt_protect(ctx, 1, 0)
+        g = C.ckpt_geometry(ctx)
+        assert g["L"] > 3 * B
+        want, _, _ = oracle_image(specs, 0, g["L_star"])
+        C.ckpt_has_apply_layers(ctx, B, B)               # bucket 0: L1, bucket 1: L2, rest: L3
+        C.ckpt_window(ctx, C.CKPT_WINDOW_COMM, s)        # an all-reduce phase
+        sid = C.ckpt_snapshot(ctx, 0, s)
+        time.sleep(0.3)
+        d = C.ckpt_host_view(ctx, 1, copy=True)[0]
+        assert not d[:2 * B].any(), "Layer 1/2 buckets moved in a communication window"
+        C.ckpt_window(ctx, C.CKPT_WINDOW_COMPUTE, s)     # buckets leave in image order: bucket 0 still waits
+        time.sleep(0.3)
+        assert not C.ckpt_host_view(ctx, 1, copy=True)[0][:B].any(), "Layer 1 bucket moved outside a bubble"
+        C.ckpt_window(ctx, C.CKPT_WINDOW_BUBBLE, s)
+        C.ckpt_wait(ctx, sid)
+        assert_bytes_equal(C.ckpt_host_view(ctx, 0, copy=True)[0], want, "image after all three layers")
+        C.ckpt_has_apply_layers(ctx, 0, 0)               # everything in Layer 3
+        C.ckpt_window(ctx, 0, s)
+        sid = C.ckpt_snapshot(ctx, 0, s)
+        time.sleep(0.3)
+        assert not C.ckpt_host_view(ctx, 1, copy=True)[0].any(), "D2H while every window was closed"
+        C.ckpt_window(ctx, C.CKPT_WINDOW_COMM, s)
+        C.ckpt_wait(ctx, sid)
+        assert_bytes_equal(C.ckpt_host_view(ctx, 0, copy=True)[0], want, "image after a communication window")
     finally:
         C.ckpt_destroy(ctx)
 
