@@ -74,6 +74,12 @@ inline uint32_t *ready_row(uint32_t *flags, uint32_t j) { return flags + kFlagBy
 // ckpt_protect (the parity is allocated after the handle blobs were exchanged); a survivor
 // reads the lost member's copy there and maps it for the rebuild (rebuild_map_parity).
 constexpr uint64_t kParityHandleOff = 2048;
+// Group abort word (u32 at this byte offset of every member's flag page): a member whose
+// collective operation fails writes (its index + 1) into every peer's page; a peer blocked
+// in a host-side wait sees it within ~20 ms and fails with EPEER instead of waiting out
+// CKPT_TIMEOUT_S.  After an abort the group must be re-created.
+constexpr uint64_t kAbortOff = 1024;
+static_assert(kNumStages * kFlagStride * 4 <= kAbortOff && kAbortOff + 4 <= kParityHandleOff, "abort word placement");
 static_assert(kNumStages * kFlagStride * 4 <= kParityHandleOff, "flag lines overlap the parity handle");
 static_assert(kParityHandleOff + sizeof(cudaIpcMemHandle_t) <= kFlagBytes, "parity handle beyond the flag page");
 
@@ -174,6 +180,7 @@ struct ckpt_ctx {
     uint8_t *peer_parity[CKPT_MAX_GROUP] = {};  // mapped on first rebuild of that member
     bool peer_parity_opened[CKPT_MAX_GROUP] = {};
     bool parity_peers_mapped = false;
+    bool abort_sent = false;  // this member wrote its abort word into every peer's page
     ckpt_ctx *members[CKPT_MAX_GROUP] = {};
 
     // CE gather buffer (CKPT_OPT_CE_GATHER; local): m-1 unit streams per bucket
@@ -370,6 +377,8 @@ static inline bool rebuild_self_encode(const ckpt_ctx *c) { return !(c->opt.flag
 void clean_pad(ckpt_ctx *c, int buf);
 int check_sticky(ckpt_ctx *c);
 void make_sticky(ckpt_ctx *c, int rc);
+void group_abort(ckpt_ctx *c);
+uint32_t peer_aborted(ckpt_ctx *c);
 int host_sync(ckpt_ctx *c);
 uint64_t effective_bucket(const ckpt_ctx *c, uint64_t req);
 bool single_launch(const ckpt_ctx *c);

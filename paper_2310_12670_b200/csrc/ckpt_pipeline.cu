@@ -294,6 +294,46 @@ void make_sticky(ckpt_ctx *c, int rc) {
         c->sticky = rc;
         c->sticky_msg = g_last_error;
     }
+    group_abort(c);  // peers waiting on this member's signals fail fast instead of timing out
+}
+
+// Write (my index + 1) into every peer's abort word (IPC groups; LOCAL members share the
+// thread that failed).  Best effort: errors are ignored, the message of the failure stands.
+void group_abort(ckpt_ctx *c) {
+    if (c->abort_sent || c->transport != CKPT_GROUP_IPC || c->m < 2 || !c->grouped) return;
+    c->abort_sent = true;
+    const std::string keep = g_last_error;
+    int dev = -1;
+    cudaGetDevice(&dev);
+    cudaSetDevice(c->device);
+    cudaStream_t t = nullptr;
+    if (cudaStreamCreateWithFlags(&t, cudaStreamNonBlocking) == cudaSuccess) {
+        static const uint32_t v[CKPT_MAX_GROUP] = {1, 2, 3, 4, 5, 6, 7, 8};
+        for (uint32_t j = 0; j < c->m; ++j)
+            if (j != c->me && c->peer_flags[j])
+                cudaMemcpyAsync((uint8_t *)c->peer_flags[j] + kAbortOff, &v[c->me], 4, cudaMemcpyHostToDevice, t);
+        cudaStreamSynchronize(t);
+        cudaStreamDestroy(t);
+    }
+    cudaGetLastError();
+    if (dev >= 0) cudaSetDevice(dev);
+    g_last_error = keep;
+}
+
+// (index + 1) of a peer that aborted the group, or 0.
+uint32_t peer_aborted(ckpt_ctx *c) {
+    if (c->transport != CKPT_GROUP_IPC || c->m < 2 || !c->flags) return 0;
+    uint32_t v = 0;
+    cudaStream_t t = nullptr;
+    if (cudaStreamCreateWithFlags(&t, cudaStreamNonBlocking) != cudaSuccess) {
+        cudaGetLastError();
+        return 0;
+    }
+    if (cudaMemcpyAsync(&v, (const uint8_t *)c->flags + kAbortOff, 4, cudaMemcpyDeviceToHost, t) == cudaSuccess)
+        cudaStreamSynchronize(t);
+    cudaStreamDestroy(t);
+    cudaGetLastError();
+    return v;
 }
 
 // Bucket = whole stripes ((m-1)u; A when unprotected).  With full-copy staging the
@@ -763,12 +803,18 @@ int sync_stream_timeout(ckpt_ctx *c, cudaStream_t s, const char *what) {
     double limit = 600.0;
     if (const char *e = getenv("CKPT_TIMEOUT_S")) limit = atof(e);
     auto t0 = std::chrono::steady_clock::now();
+    double next_abort_check = 0.1;
     for (;;) {
         cudaError_t e = cudaStreamQuery(s);
         if (e == cudaSuccess) return CKPT_OK;
         if (e != cudaErrorNotReady) return fail(CKPT_ECUDA, "%s: %s", what, cudaGetErrorString(e));
         double el = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
-        if (el > limit) {
+        uint32_t ab = 0;
+        if (el > next_abort_check) {  // a peer's collective failed: it will never signal
+            next_abort_check = el + 0.02;
+            ab = peer_aborted(c);
+        }
+        if (ab || el > limit) {
             // snapshot of the flag page for the message, then release our own stream
             // waits so the context can be destroyed
             uint32_t f[kNumStages * kFlagStride] = {};
@@ -785,8 +831,13 @@ int sync_stream_timeout(ckpt_ctx *c, cudaStream_t s, const char *what) {
                 for (uint32_t j = 0; j < c->m && o < (int)sizeof buf; ++j)
                     o += snprintf(buf + o, sizeof buf - o, "%u%s", f[st * kFlagStride + j], j + 1 < c->m ? "," : "]");
             }
-            cudaMemset(c->flags, 0x7f, kFlagAlloc);
+            cudaMemset(c->flags, 0x7f, kAbortOff);  // release our waits: the REL/DONE lines
+            cudaMemset((uint8_t *)c->flags + kFlagBytes, 0x7f, kFlagAlloc - kFlagBytes);  // and the READY rows
             cudaGetLastError();
+            if (ab) {
+                c->abort_sent = true;  // the group is gone: do not echo the abort
+                return fail(CKPT_EPEER, "%s: member %u aborted the group (member %u: %s)", what, ab - 1, c->me, buf);
+            }
             return fail(CKPT_EPEER, "%s: timed out after %.0f s waiting for peers (member %u: %s)", what, limit, c->me, buf);
         }
         if (el < 0.002) {  // the first 2 ms: poll without sleeping (small snapshots)

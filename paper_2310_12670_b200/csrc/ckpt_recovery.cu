@@ -166,8 +166,11 @@ int rebuild_aec(ckpt_ctx *c, int32_t lost, void *stream) {
     if (rc) return rc;
     if (c->pending_id || c->requested) return fail(CKPT_ESTATE, "rebuild: a snapshot is in flight");
     const uint32_t kl = (uint32_t)lost;
-    if (c->me != kl && c->completed < 0)
-        return fail(CKPT_EUNRECOVERABLE, "rebuild: survivor %u has no completed image (more than one loss)", c->me);
+    if (c->me != kl && c->completed < 0) {
+        rc = fail(CKPT_EUNRECOVERABLE, "rebuild: survivor %u has no completed image (more than one loss)", c->me);
+        group_abort(c);  // the other members would wait for this survivor's share forever
+        return rc;
+    }
     if ((rc = set_dev(c))) return rc;
     cudaStream_t caller = (cudaStream_t)stream;
     const uint64_t B = effective_bucket(c, 0);
@@ -216,7 +219,10 @@ int rebuild_aec(ckpt_ctx *c, int32_t lost, void *stream) {
         return rc;
     }
     // IPC: every member runs its own side; the version is the survivors' completed id
-    if ((!rebuild_self_encode(c) && (rc = rebuild_map_parity(c, kl))) || (rc = prepare_op(c, B))) return rc;
+    if ((!rebuild_self_encode(c) && (rc = rebuild_map_parity(c, kl))) || (rc = prepare_op(c, B))) {
+        make_sticky(c, rc);  // aborts the group: the peers fail fast instead of timing out
+        return rc;
+    }
     CUDA_TRY(cudaEventRecord(c->ev_capture, caller));
     CUDA_TRY(cudaStreamWaitEvent(c->sC, c->ev_capture, 0));
     CUDA_TRY(cudaStreamWaitEvent(c->sX, c->ev_capture, 0));

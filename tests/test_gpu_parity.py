@@ -819,15 +819,22 @@ def test_c_program_drill(torch, C, tmp_path, m, lost):
     assert r.stdout.strip() == f"ok m={m} lost={lost}"
 
 
-@pytest.mark.parametrize("impl", ["lsu", "tma"])
-def test_smoke_with_each_xor_kernel(torch, C, impl):
-    """Both XOR implementations (CKPT_XOR_IMPL is read once per process, hence a subprocess):
-    __graft_entry__.smoke() -- m=4 snapshot + parity, rebuild, load -- bit-exact vs the oracle."""
+@pytest.mark.parametrize("knob", ["CKPT_XOR_IMPL=lsu", "CKPT_XOR_IMPL=tma", "CKPT_XOR_TILE=1", "CKPT_XOR_TILE=2",
+                                  "CKPT_PACK_WAVES=1", "CKPT_PACK_WAVES=64", "CKPT_XOR_CTAS=296"])
+def test_every_tuning_knob_stays_bit_exact(torch, C, knob):
+    """Every environment tuning knob (read once per process, hence a subprocess) under the
+    group encode and drill parity tests (every m, unit, staging mode and flag set, incl. the
+    push encode) and the smoke (snapshot + parity, rebuild, load): bit-exact vs the oracle."""
     import os
     import subprocess
     import sys
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    env = dict(os.environ, CKPT_XOR_IMPL=impl)
+    k, v = knob.split("=")
+    env = dict(os.environ, **{k: v})
+    r = subprocess.run([sys.executable, "-m", "pytest", "-x", "-q", "-m", "gpu", os.path.join(root, "tests", "test_gpu_parity.py"),
+                        "-k", "group_encode_matches_oracle or group_drill_rebuild_every_rank or push_encode_repeated"],
+                       cwd=root, env=env, capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0 and " passed" in r.stdout, r.stdout[-3000:] + r.stderr[-2000:]
     r = subprocess.run([sys.executable, os.path.join(root, "__graft_entry__.py"), "smoke"], cwd=root, env=env,
                        capture_output=True, text=True, timeout=300)
     assert r.returncode == 0 and "smoke ok" in r.stdout, r.stdout[-2000:] + r.stderr[-2000:]

@@ -660,3 +660,84 @@ def test_group_restart_reattaches_over_ipc(drop):
         _run_fn(functools.partial(_persist_worker, "read", key, drop), world)
     finally:
         C.ckpt_arena_unlink(key, world, 2)
+
+
+def test_torchrun_elastic_replaces_a_killed_rank(tmp_path):
+    """REFT-load after a real process failure under torchrun's elastic agent (P.545,
+    P.551-555; SPEC S.514): rank N-1 loses its host memory and dies after v2 committed; the
+    agent (--max-restarts 1) restarts the group, the new processes re-attach the persistent
+    arenas, recover the replaced member from parity and load v2 bit-exactly
+    (tools/elastic_drill.py)."""
+    import json
+    import random
+    import subprocess
+    import sys
+    world = min(_world(), 4)
+    from paper_2310_12670_b200 import ckpt as C
+    key = random.getrandbits(48) | 1
+    port = _free_port()
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes", "1", "--nproc-per-node", str(world),
+           "--max-restarts", "1", "--master-addr", "127.0.0.1", "--master-port", str(port),
+           os.path.join(root, "tools", "elastic_drill.py"), "--key", hex(key), "--out", str(tmp_path)]
+    env = dict(os.environ, CKPT_TIMEOUT_S="120")
+    try:
+        r = subprocess.run(cmd, cwd=root, env=env, capture_output=True, text=True, timeout=600)
+        assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+        res = [json.load(open(tmp_path / f"rank{j}.json")) for j in range(world)]
+        for x in res:
+            assert x["attempt"] == 1, x       # the group was restarted once by the agent
+            assert x["ok"], x
+    finally:
+        C.ckpt_arena_unlink(key, world, 2)
+
+
+def _abort_worker(rank, world, port, q):
+    """Member 0 cannot serve a rebuild (it has no completed image): its failure aborts the
+    group, so the member waiting for it fails with EPEER in seconds, not after the timeout."""
+    try:
+        os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank), WORLD_SIZE=str(world))
+        import time
+
+        import torch
+        import torch.distributed as dist
+
+        from paper_2310_12670_b200 import ckpt as C
+        from synth.gpu import descriptors, make_rank_state
+
+        torch.cuda.set_device(rank)
+        dev = torch.device("cuda", rank)
+        dist.init_process_group("nccl", device_id=dev)
+        specs, ts = make_rank_state("tiny_7", rank, dev)
+        ctx = C.ckpt_create(rank, C.ckpt_options_default(n_slots=0, bucket_bytes=1 << 16, stripe_unit=4096))
+        C.ckpt_register(ctx, descriptors(ts, specs))
+        C.protect_ipc(ctx)
+        sid = C.ckpt_snapshot(ctx)
+        C.ckpt_wait(ctx, sid)
+        if rank == 0:
+            C.ckpt_forget(ctx, 0xA5)         # a second loss: no survivor image to serve
+        dist.barrier()
+        t0 = time.time()
+        code = 0
+        try:
+            C.ckpt_rebuild(ctx, world - 1)
+        except C.CkptError as e:
+            code = e.code
+        el = time.time() - t0
+        want = C.CKPT_EUNRECOVERABLE if rank == 0 else (C.CKPT_EPEER if rank == world - 1 else code)
+        ok = [code == want, el < 30.0]
+        C.ckpt_destroy(ctx)
+        dist.destroy_process_group()
+        q.put((rank, ok, None))
+    except Exception:
+        q.put((rank, None, traceback.format_exc()))
+
+
+def test_failed_member_aborts_the_group_fast():
+    """a survivor that fails before its share of a collective rebuild must not
+    leave its peers blocked until CKPT_TIMEOUT_S (here 300 s): the abort word releases them."""
+    os.environ["CKPT_TIMEOUT_S"] = "300"
+    try:
+        _run_fn(_abort_worker, min(_world(), 2), timeout=200)
+    finally:
+        os.environ["CKPT_TIMEOUT_S"] = "90"
