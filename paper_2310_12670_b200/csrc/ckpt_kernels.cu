@@ -592,21 +592,15 @@ constexpr int xor_unroll() { return N == 1 ? 8 : N == 2 ? 4 : N == 3 ? 3 : 2; }
 // bytes of peer reads in flight (~48 KiB, ~190 KiB per SM) with one instruction per
 // segment instead of one per 16 B.  Segments past an input's `valid` are not loaded and
 // read as zero (reading Q5).
-// Tile T, NS stages, W warps per CTA (NS * NIN * T per warp, <= 192 KiB per CTA).  The
-// default takes 16 KiB bulk pieces for m <= 5 (8 KiB beyond): the piece size, not the bytes
-// in flight, sets the NVLink pull rate -- at m = 4, 4 KiB pieces reached 616 GB/s against
-// 675 GB/s for the all-concurrent 16 KiB probe (CKPT_XOR_TILE selects the older 4-warp
-// configurations for A/B: 1 = small pieces, 2 = 8 KiB x 2 warps).
-template <int NIN, int CFG>
+// Tile T, NS stages, W = 4 warps per CTA: NS * NIN * T <= 48 KiB per warp.  Round-2 A/B
+// (tools/r02_xor_ab.sh, m = 4, C2): 16 KiB pieces on 1-2 warps per CTA moved the same
+// 606-614 GB/s as these 4 KiB pieces on 4 warps (611-614), and 64 CTAs the same as 32.
+template <int NIN>
 struct XorTmaCfg {
-    static constexpr uint32_t T = CFG == 1 ? (NIN == 1 ? 16384 : NIN == 2 ? 8192 : NIN <= 4 ? 4096 : 2048)
-                                : CFG == 2 ? (NIN <= 2 ? 16384 : 8192)
-                                           : (NIN <= 4 ? 16384 : 8192);
-    static constexpr int W = CFG == 1 ? 4 : CFG == 2 ? (NIN == 1 ? 4 : NIN <= 4 ? 2 : 1) : (NIN == 1 ? 4 : NIN == 2 ? 2 : 1);
-    static constexpr int NS0 = (int)((192u * 1024u) / (T * NIN * W));
-    static constexpr int NS = NS0 > 6 ? 6 : NS0;
+    static constexpr uint32_t T = NIN == 1 ? 16384 : NIN == 2 ? 8192 : NIN <= 4 ? 4096 : 2048;
+    static constexpr int NS = (int)((48u * 1024u) / (T * NIN)) > 6 ? 6 : (int)((48u * 1024u) / (T * NIN));
+    static constexpr int W = 4;
     static constexpr int smem = W * NS * NIN * (int)T;
-    static_assert(NS >= 2 && smem <= 200 * 1024, "XOR TMA configuration");
 };
 
 template <int NIN>
@@ -624,9 +618,9 @@ __device__ __forceinline__ void xor_tile_geometry(const XorArgs &a, uint64_t t, 
     }
 }
 
-template <int NIN, int CFG>
-__global__ void __launch_bounds__(32 * XorTmaCfg<NIN, CFG>::W) xor_tma_kernel(const __grid_constant__ XorArgs a) {
-    using Cfg = XorTmaCfg<NIN, CFG>;
+template <int NIN>
+__global__ void __launch_bounds__(32 * XorTmaCfg<NIN>::W) xor_tma_kernel(const __grid_constant__ XorArgs a) {
+    using Cfg = XorTmaCfg<NIN>;
     constexpr uint32_t T = Cfg::T;
     constexpr int NS = Cfg::NS, W = Cfg::W;
     extern __shared__ __align__(128) uint8_t smem[];
@@ -704,34 +698,22 @@ cudaError_t launch_xor_n(const XorArgs &a, int max_ctas, cudaStream_t s) {
     return cudaGetLastError();
 }
 
-template <int N, int CFG>
-cudaError_t launch_xor_tma_cfg(const XorArgs &a, int ctas, cudaStream_t s) {
-    using Cfg = XorTmaCfg<N, CFG>;
+template <int N>
+cudaError_t launch_xor_tma_n(const XorArgs &a, int ctas, cudaStream_t s) {
+    using Cfg = XorTmaCfg<N>;
     static unsigned long long attr_set = 0;  // bit d: attribute set on device d
     int dev = 0;
     cudaGetDevice(&dev);
     if (!(attr_set & (1ull << dev))) {
-        cudaError_t e = cudaFuncSetAttribute(xor_tma_kernel<N, CFG>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::smem);
+        cudaError_t e = cudaFuncSetAttribute(xor_tma_kernel<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::smem);
         if (e != cudaSuccess) return e;
         attr_set |= 1ull << dev;
     }
     const uint64_t ntiles = a.nstripes * ((a.unit + Cfg::T - 1) / Cfg::T);
     const uint64_t need = (ntiles + Cfg::W - 1) / Cfg::W;
     const int grid = (int)(need < (uint64_t)ctas ? need : (uint64_t)ctas);
-    xor_tma_kernel<N, CFG><<<grid, 32 * Cfg::W, Cfg::smem, s>>>(a);
+    xor_tma_kernel<N><<<grid, 32 * Cfg::W, Cfg::smem, s>>>(a);
     return cudaGetLastError();
-}
-
-template <int N>
-cudaError_t launch_xor_tma_n(const XorArgs &a, int ctas, cudaStream_t s) {
-    static int cfg = -1;
-    if (cfg < 0) {
-        const char *e = getenv("CKPT_XOR_TILE");
-        cfg = e ? std::max(0, std::min(2, atoi(e))) : 0;
-    }
-    if (cfg == 1) return launch_xor_tma_cfg<N, 1>(a, ctas, s);
-    if (cfg == 2) return launch_xor_tma_cfg<N, 2>(a, ctas, s);
-    return launch_xor_tma_cfg<N, 0>(a, ctas, s);
 }
 
 // ---------------------------------------------------------------------------------
@@ -904,15 +886,9 @@ cudaError_t preload_kernels() {
         (const void *)xor_kernel<3, xor_unroll<3>()>, (const void *)xor_kernel<4, xor_unroll<4>()>,
         (const void *)xor_kernel<5, xor_unroll<5>()>, (const void *)xor_kernel<6, xor_unroll<6>()>,
         (const void *)xor_kernel<7, xor_unroll<7>()>, (const void *)xor_kernel<8, xor_unroll<8>()>,
-        (const void *)xor_tma_kernel<1, 0>, (const void *)xor_tma_kernel<2, 0>, (const void *)xor_tma_kernel<3, 0>,
-        (const void *)xor_tma_kernel<4, 0>, (const void *)xor_tma_kernel<5, 0>, (const void *)xor_tma_kernel<6, 0>,
-        (const void *)xor_tma_kernel<7, 0>, (const void *)xor_tma_kernel<8, 0>,
-        (const void *)xor_tma_kernel<1, 1>, (const void *)xor_tma_kernel<2, 1>, (const void *)xor_tma_kernel<3, 1>,
-        (const void *)xor_tma_kernel<4, 1>, (const void *)xor_tma_kernel<5, 1>, (const void *)xor_tma_kernel<6, 1>,
-        (const void *)xor_tma_kernel<7, 1>, (const void *)xor_tma_kernel<8, 1>,
-        (const void *)xor_tma_kernel<1, 2>, (const void *)xor_tma_kernel<2, 2>, (const void *)xor_tma_kernel<3, 2>,
-        (const void *)xor_tma_kernel<4, 2>, (const void *)xor_tma_kernel<5, 2>, (const void *)xor_tma_kernel<6, 2>,
-        (const void *)xor_tma_kernel<7, 2>, (const void *)xor_tma_kernel<8, 2>,
+        (const void *)xor_tma_kernel<1>, (const void *)xor_tma_kernel<2>, (const void *)xor_tma_kernel<3>,
+        (const void *)xor_tma_kernel<4>, (const void *)xor_tma_kernel<5>, (const void *)xor_tma_kernel<6>,
+        (const void *)xor_tma_kernel<7>, (const void *)xor_tma_kernel<8>,
         (const void *)probe_pull_kernel, (const void *)xor_push_kernel};
     for (const void *f : fns) {
         cudaError_t e = cudaFuncGetAttributes(&fa, f);
