@@ -11,4 +11,5 @@ timeout 300 $X > gpurun_out/r02_xor_m4_plain.log 2>&1
 timeout 900 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum,nvlrx__bytes.sum,nvlrx__bytes_data_user.sum,nvltx__bytes.sum,nvltx__bytes_data_user.sum --clock-control none -k regex:xor_tma -c 8 --csv --log-file gpurun_out/r02_xortma_m4_nvlink.csv $X > gpurun_out/r02_ncu_xor_m4_metrics.log 2>&1
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:'pack|xor' -c 200 --csv --log-file gpurun_out/r02_xortma_m4_launches.csv $X > gpurun_out/r02_ncu_xor_m4_launch.log 2>&1
 timeout 1200 ncu --set full --clock-control none --import-source on -k regex:xor_tma -s 4 -c 1 -o gpurun_out/prof_r02_xortma_m4 $X > gpurun_out/r02_ncu_xor_m4_full.log 2>&1
+N=4 CFG=c5_13b_drill LOST=0,3 timeout 1200 bash tools/rb_share_ab.sh > gpurun_out/r02_rb_share_ab_m4.log 2>&1
 ls -la gpurun_out
