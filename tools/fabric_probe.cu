@@ -12,6 +12,9 @@
 //   sm_red    kernel: cp.async.bulk G->S locally, cp.reduce.async.bulk .xor.b64 into the
 //             peers (the push-mode encode's transfer); checked: dst ^= src
 //   lsu_push  kernel: 128-bit ld.global.nc locally, st.global into the peers
+//   xorpat4k / xorpat16k (m = 4): the encode's load pattern -- each stage holds one segment
+//             from EVERY peer (unit sigma(me, j) of a stripe), one mbarrier for all three --
+//             with xor_tma_kernel's 4 KiB x 4 warps or 16 KiB x 1 warp geometry, no arithmetic
 // Reports per GPU: GB/s of NVLink bytes out (push) or in (pull), min over GPUs, and the
 // aggregate.  Timing: CUDA events per GPU, best of `reps`, all GPUs launched back to back.
 //
@@ -130,6 +133,47 @@ __global__ void __launch_bounds__(32 * kW) bulk_kernel(const __grid_constant__ A
     }
 }
 
+
+// The encode's load pattern without its arithmetic: tile t of unit-space (stripe s, piece w
+// of a unit) needs one T-byte segment from EACH peer (unit sigma(me, j) of stripe s) in one
+// stage, completed by one mbarrier (all m-1 must land before the stage is reused) -- as in
+// xor_tma_kernel.  Data discarded.
+template <int NIN, uint32_t T, int NS, int W>
+__global__ void __launch_bounds__(32 * W) xorpat_kernel(const __grid_constant__ Args a, uint64_t unit, uint32_t me) {
+    extern __shared__ __align__(128) uint8_t smem[];
+    __shared__ __align__(8) uint64_t bars[W][NS];
+    const uint32_t lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    if (lane) return;
+    uint8_t *ring = smem + (size_t)w * NS * NIN * T;
+    for (int i = 0; i < NS; ++i) mbar_init(&bars[w][i]);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    // every peer's staging holds n * NIN bytes = n / unit stripes of NIN units
+    const uint64_t stripe = unit * NIN, nstripes = a.n * NIN / stripe, tpu = unit / T;
+    const uint64_t items = nstripes * tpu, step = (uint64_t)gridDim.x * W;
+    auto issue = [&](uint64_t it, int st) {
+        const uint64_t sidx = it / tpu, off = (it - sidx * tpu) * T;
+        mbar_expect_tx(&bars[w][st], T * NIN);
+        for (int k = 0; k < NIN; ++k) {
+            const uint32_t j = (uint32_t)k + ((uint32_t)k >= me ? 1u : 0u);  // peer j (skip me)
+            const uint32_t sig = me - (me > j ? 1u : 0u);                     // sigma(me, j)
+            g2s(ring + ((size_t)st * NIN + k) * T, a.src[k] + sidx * stripe + sig * unit + off, T, &bars[w][st]);
+        }
+    };
+    const uint64_t first = (uint64_t)blockIdx.x * W + w;
+    int k = 0;
+    for (uint64_t it = first; it < items && k < NS; it += step, ++k) issue(it, k);
+    uint32_t phase = 0;
+    int st = 0;
+    for (uint64_t it = first; it < items; it += step) {
+        mbar_wait(&bars[w][st], (phase >> st) & 1);
+        phase ^= 1u << st;
+        const uint64_t nx = it + (uint64_t)NS * step;
+        if (nx < items) issue(nx, st);
+        st = st + 1 == NS ? 0 : st + 1;
+    }
+}
+
 __global__ void __launch_bounds__(256) lsu_push_kernel(const Args a) {
     const uint64_t words = a.n / 16;
     const uint64_t total = words * a.npeers;
@@ -239,7 +283,20 @@ int main(int argc, char **argv) {
                     RT(cudaEventDestroy(j));
                 }
             }
-            if (mode == "sm_pull" || mode == "sm_push" || mode == "sm_red")
+            if (mode == "xorpat4k" || mode == "xorpat16k") {  // needs m = 4; src[q] = peer staging base
+                Args b = a;
+                int q2 = 0;
+                for (int p = 0; p < m; ++p)
+                    if (p != d) b.src[q2++] = src[p];
+                b.n = n;  // per peer: n bytes pulled; each peer's buffer holds n*m >= n*(m-1) bytes
+                if (mode == "xorpat4k") {
+                    RT(cudaFuncSetAttribute(xorpat_kernel<3, 4096, 4, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 4 * 4 * 3 * 4096));
+                    xorpat_kernel<3, 4096, 4, 4><<<ctas, 128, 4 * 4 * 3 * 4096, st[d * m]>>>(b, 65536, (uint32_t)d);
+                } else {
+                    RT(cudaFuncSetAttribute(xorpat_kernel<3, 16384, 4, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 4 * 3 * 16384));
+                    xorpat_kernel<3, 16384, 4, 1><<<ctas, 32, 4 * 3 * 16384, st[d * m]>>>(b, 65536, (uint32_t)d);
+                }
+            } else if (mode == "sm_pull" || mode == "sm_push" || mode == "sm_red")
                 bulk_kernel<<<ctas, 32 * kW, kW * kNS * kT, st[d * m]>>>(a);
             else if (mode == "lsu_push")
                 lsu_push_kernel<<<ctas, 256, 0, st[d * m]>>>(a);

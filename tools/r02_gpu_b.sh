@@ -2,6 +2,9 @@
 # --set full capture of the N=1 pack, and the NVLink counters + --set full capture of the
 # m = 4 XOR encode (one process drives 4 GPUs: tools/xor_local2.py).
 set -x
+nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -o /tmp/fabric tools/fabric_probe.cu
+for mode in sm_pull xorpat4k xorpat16k; do for c in 32 64; do timeout 60 /tmp/fabric 4 1536 $mode $c 5 >> gpurun_out/r02_fabric_b.jsonl 2>>gpurun_out/r02_fabric_b.err; done; done
+for c in 16 32; do CKPT_XOR_CTAS=$c timeout 300 python tools/xor_local2.py --m 4 --reps 3 >> gpurun_out/r02_xor_fewctas.jsonl 2>>gpurun_out/r02_xor_fewctas.err; done
 timeout 600 python bench.py > gpurun_out/r02_bench_n1.jsonl 2> gpurun_out/r02_bench_n1.err
 timeout 900 python -m torch.distributed.run --nnodes 1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29611 bench.py --gpus 2 > gpurun_out/r02_bench_n2.jsonl 2> gpurun_out/r02_bench_n2.err
 timeout 900 python -m torch.distributed.run --nnodes 1 --nproc-per-node 4 --master-addr 127.0.0.1 --master-port 29612 bench.py --gpus 4 > gpurun_out/r02_bench_n4.jsonl 2> gpurun_out/r02_bench_n4.err
