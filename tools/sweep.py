@@ -35,6 +35,8 @@ def main():
     p.add_argument("--scheme", type=int, default=0, help="CKPT_SCHEME_*: 1 AEC, 2 ARC, 3 ARC+AEC")
     p.add_argument("--host-buffers", type=int, default=2)
     p.add_argument("--corun", action="store_true", help="bf16 GEMM co-run slowdown per bucket size (bench.py's)")
+    p.add_argument("--max-ctas", default="0",
+                   help="comma list of CTA budgets of the pack/XOR launches (0 = 2 x SMs); one record per budget")
     a = p.parse_args()
     import torch
     import torch.distributed as dist
@@ -62,13 +64,13 @@ def main():
 
     specs, ts = make_rank_state(a.config, rank, dev)
     S = sum(s.nbytes for s in specs)
-    for bmib in [int(x) for x in a.buckets.split(",")]:
+    for bmib, mc in [(int(x), int(y)) for x in a.buckets.split(",") for y in a.max_ctas.split(",")]:
         flags = a.flags | C.CKPT_OPT_TIMING | (C.CKPT_OPT_DEVICE_ONLY if a.device_only else 0)
         if a.scheme in (2, 3):
             flags |= C.CKPT_OPT_SHM_ARENA
         n_slots = 0 if a.device_only else a.n_slots
         ctx = C.ckpt_create(local, C.ckpt_options_default(bucket_bytes=bmib << 20, n_slots=n_slots,
-                                                          stripe_unit=a.unit, flags=flags,
+                                                          stripe_unit=a.unit, flags=flags, max_ctas=mc,
                                                           host_buffers=a.host_buffers))
         C.ckpt_register(ctx, descriptors(ts, specs))
         if world > 1:
@@ -92,6 +94,7 @@ def main():
         st = C.ckpt_get_stats(ctx)
         t = statistics.median(times)
         rec = {"config": a.config, "m": g["m"], "bucket_mib": bmib, "n_slots": n_slots, "flags": flags,
+               "max_ctas": mc or "2 x SMs",
                "state_bytes": S, "L_star": g["L_star"], "snapshot_ms": round(t * 1e3, 3),
                "state_gbs_per_gpu": round(S / t / 1e9, 3), "wire_gbs_per_gpu": round(st["d2h_bytes"] / a.reps / t / 1e9, 3),
                "pack_us_per_launch": round(st["pack_ms"] / max(st["pack_launches"], 1) * 1e3, 2),
@@ -104,7 +107,7 @@ def main():
             import bench
             co = bench.gemm_corun(torch, C, ctx, st0, bmib << 20, bar, amax, dev)
             rec["gemm_slowdown_pct"] = co["slowdown_pct"]
-            rec["snapshot_ms_while_corunning"] = co["snapshot_ms_while_corunning"]
+            rec["gemm_corun"] = {k: co[k] for k in ("whole_window", "pack_window", "protect_window", "snapshot_window")}
         if a.drill and g["m"] >= 2:
             lost = [tuple(int(y) for y in x.split("+")) for x in a.lost.split(",")] if a.lost else [(0,), (g["m"] - 1,)]
             C.ckpt_stats_reset(ctx)
