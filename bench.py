@@ -452,10 +452,25 @@ def main():
         roof["traffic_source"] = os.path.relpath(tr_path, ROOT) if tr else None
         for k in ("achieved", "frac", "avg_launch_us"):
             roof[k] = round(roof[k], 4)
+    # m = 2 with the copy-engine gather: the parity is a mirror (P.459) pulled by the copy
+    # engine straight into the parity buffer -- no kernel, so not a roofline candidate;
+    # reported against the live all-concurrent copy-engine pull probe
+    ce_mirror = None
+    if st.get("gather_ops") and st["gather_ms"] > 0:
+        per_step = g["L_star"]
+        dur = st["gather_ms"] / max(1, st["snapshots"])
+        live = fabric.get("ce_pull_gbs_min_over_ranks") if fabric else None
+        ce_mirror = {"bound": "nvlink", "engine": "copy engine (cudaMemcpyAsync peer -> parity), zero SMs",
+                     "achieved": round(per_step / dur / 1e6, 2), "peak": live or NVLINK_PEAK_GBS,
+                     "unit": "GB/s", "bytes_per_snapshot": per_step, "ms_per_snapshot": round(dur, 3),
+                     "copies_per_snapshot": st["gather_ops"] // max(1, st["snapshots"]),
+                     "peak_source": "live all-concurrent copy-engine pull probe (ckpt_probe_fabric ce_pull, min over "
+                                    "ranks), this run" if live else "B200_PROFILING.md 770 GB/s"}
+        ce_mirror["frac"] = round(ce_mirror["achieved"] / ce_mirror["peak"], 4)
     # E9 analog (P.469: erasure coding at 12-15x the snapshot rate): the XOR encode's
     # in-situ NVLink GB/s over this rank's host-link (D2H wire) GB/s
     e9 = None
-    xk = [d for k, _, d in kern if k == "xor"]
+    xk = [d for k, _, d in kern if k == "xor"] or ([ce_mirror] if ce_mirror else [])
     if xk and wire > 0:
         e9 = {"value": round(xk[0]["achieved"] / wire, 2), "xor_gbs": round(xk[0]["achieved"], 1),
               "d2h_wire_gbs": round(wire, 2), "paper": "12-15x (P.469)"}
@@ -544,7 +559,7 @@ def main():
             "host_link": None if a.device_only else {
                 "achieved_wire_gbs_rank0": round(wire, 3), "peak_d2h_gbs_rank0_measured": round(d2h_peak, 3),
                 "frac": round(wire / d2h_peak, 4), "note": "binding roofline of the whole step: pinned D2H of data + parity"},
-            "roofline": roof, "other_kernels": others,
+            "roofline": roof, "other_kernels": others, "ce_mirror": ce_mirror,
             "gpu_launches": launches,
             "clocks": clocks,
             "e2e": e2e, "cpu_baseline": cpu, "gemm_corun": corun,

@@ -68,7 +68,9 @@ extern "C" {
 #define CKPT_OPT_CE_PACK     0x8u  /* pack/unpack with copy-engine D2D copies (zero SMs)  */
 #define CKPT_OPT_CE_GATHER   0x10u /* parity: copy engines pull the m-1 peer units over
                                       NVLink (2-D copies) into local HBM, then the XOR
-                                      kernel runs locally at HBM speed (few SM-seconds)  */
+                                      kernel runs locally at HBM speed (few SM-seconds);
+                                      at m = 2 (a mirror, P.459) the pull lands in the
+                                      parity buffer itself: no kernel, zero SMs           */
 #define CKPT_OPT_DEVICE_ONLY 0x20u /* keep the image in HBM only: snapshot = pack + parity
                                       into the full device staging (n_slots must be 0), no
                                       D2H, no host arena; load/rebuild work from HBM.  A
@@ -198,6 +200,9 @@ typedef struct ckpt_stats {      /* cumulative since ckpt_stats_reset           
                                     (only with CKPT_OPT_TIMING)                          */
     double   last_snapshot_ms;   /* capture event -> last D2H event of the last snapshot
                                     (only with CKPT_OPT_TIMING)                          */
+    uint64_t gather_ops;         /* m = 2 with CKPT_OPT_CE_GATHER: copy-engine mirror
+                                    pulls (one per bucket), no XOR kernel                */
+    double   gather_ms;          /* their summed durations (only with CKPT_OPT_TIMING)   */
 } ckpt_stats;
 
 /* ---- lifecycle ------------------------------------------------------------------------- */

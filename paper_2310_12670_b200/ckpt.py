@@ -82,7 +82,8 @@ class ckpt_stats(ctypes.Structure):
                                     "unpack_launches", "rebuild_launches", "pack_bytes", "xor_bytes_in",
                                     "xor_bytes_out", "d2h_bytes", "h2d_bytes", "ce_copies", "rebuild_bytes_in",
                                     "rebuild_bytes_out")] + \
-               [(n, ctypes.c_double) for n in ("pack_ms", "xor_ms", "unpack_ms", "rebuild_ms", "last_snapshot_ms")]
+               [(n, ctypes.c_double) for n in ("pack_ms", "xor_ms", "unpack_ms", "rebuild_ms", "last_snapshot_ms")] + \
+               [("gather_ops", _u64), ("gather_ms", ctypes.c_double)]
 
     def as_dict(self):
         return {n: getattr(self, n) for n, _ in self._fields_}

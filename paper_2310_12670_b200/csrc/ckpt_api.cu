@@ -704,7 +704,7 @@ extern "C" int ckpt_protect(ckpt_ctx *c, const ckpt_group *g) {
         CUDA_TRY(cudaIpcGetMemHandle(&h, c->parity));
         CUDA_TRY(cudaMemcpy((uint8_t *)c->flags + kParityHandleOff, &h, sizeof h, cudaMemcpyHostToDevice));
     }
-    if (c->aec && (c->opt.flags & CKPT_OPT_CE_GATHER)) {
+    if (c->aec && (c->opt.flags & CKPT_OPT_CE_GATHER) && m > 2) {  // m = 2: pulled into the parity
         c->gather_bytes = c->full_copy ? std::max<uint64_t>(Lstar, 4096) : c->parity_bytes * (m - 1);
         if (cudaMalloc(&c->gather, c->gather_bytes) != cudaSuccess) {
             cudaGetLastError();

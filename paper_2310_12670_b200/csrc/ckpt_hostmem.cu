@@ -53,6 +53,7 @@ int harvest_timing(ckpt_ctx *c) {
             case 0: c->st.pack_ms += ms; break;
             case 1: c->st.xor_ms += ms; break;
             case 2: c->st.unpack_ms += ms; break;
+            case 4: c->st.gather_ms += ms; break;
             default: c->st.rebuild_ms += ms; break;
         }
     }

@@ -115,7 +115,7 @@ struct Segment {
 
 struct TimedLaunch {
     cudaEvent_t a, b;
-    int kind;  // 0 pack 1 xor 2 unpack 3 rebuild
+    int kind;  // 0 pack 1 xor 2 unpack 3 rebuild 4 CE mirror gather
 };
 
 enum HostKind { kNone = 0, kCudaHost = 1, kAnon = 2, kShmOwn = 3, kShmPeer = 4, kView = 5 };

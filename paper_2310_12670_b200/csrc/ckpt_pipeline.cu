@@ -428,11 +428,15 @@ int stage_pack(ckpt_ctx *c, uint64_t k) {
 }
 
 
+// m = 2 is a mirror (Eq 1 with one term: P_r = D_{1-r}, zero-padded to L*, P.459): the
+// copy engine pulls the peer's bucket straight into the parity slot and no XOR kernel runs.
+bool ce_mirror(const ckpt_ctx *c) { return c->m == 2 && c->aec && (c->opt.flags & CKPT_OPT_CE_GATHER); }
+
 int do_gather_ce(ckpt_ctx *c, uint64_t k, cudaStream_t s) {
     const uint64_t bb = bucket_begin(c, k), be = bucket_end(c, k);
     const uint64_t u = c->unit, pitch = (uint64_t)(c->m - 1) * u, nst = (be - bb) / pitch;
     const uint64_t gs = gather_stride(c, k);
-    uint8_t *g = gather_slot_ptr(c, k);
+    uint8_t *g = ce_mirror(c) ? parity_slot_ptr(c, k) : gather_slot_ptr(c, k);
     uint32_t jj = 0;
     for (uint32_t j = 0; j < c->m; ++j) {
         if (j == c->me) continue;
@@ -563,6 +567,16 @@ int stage_xor(ckpt_ctx *c, uint64_t k) {
     if (c->opt.flags & CKPT_OPT_CE_GATHER) {
         if ((rc = wait_all(c, c->sG, kReady, bucket_seq(c, k), s))) return rc;
         if (ring_reuse(c, k)) CUDA_TRY(cudaStreamWaitEvent(c->sG, c->ev_xored[s], 0));
+        if (ce_mirror(c)) {  // the gathered unit IS the parity: no XOR kernel
+            if (ring_reuse(c, k)) CUDA_TRY(cudaStreamWaitEvent(c->sG, c->ev_d2h_par[s], 0));
+            TimedLaunch *t;
+            if ((rc = timed_begin(c, c->sG, 4, &t))) return rc;
+            if ((rc = do_gather_ce(c, k, c->sG))) return rc;
+            if ((rc = timed_end(t, c->sG))) return rc;
+            c->st.gather_ops++;
+            CUDA_TRY(cudaEventRecord(c->ev_xored[s], c->sG));
+            return sig_signal(c, c->sG, kRel, bucket_seq(c, k), s);
+        }
         if ((rc = do_gather_ce(c, k, c->sG))) return rc;
         CUDA_TRY(cudaEventRecord(c->ev_gathered[s], c->sG));
         if ((rc = sig_signal(c, c->sG, kRel, bucket_seq(c, k), s))) return rc;

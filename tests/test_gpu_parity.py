@@ -217,7 +217,9 @@ def test_group_encode_matches_oracle(torch, C, m, unit, n_slots, bucket, flags):
                                                   (8, 1024, 3, 0x200), (3, 4096, 0, 0x280), (7, 16, 0, 0x200),
                                                   # CKPT_OPT_XOR_PUSH: push-mode encode (bulk XOR reductions)
                                                   (2, 4096, 0, 0x400), (4, 65536, 0, 0x402), (8, 1024, 0, 0x600),
-                                                  (5, 16, 0, 0x480)])
+                                                  (5, 16, 0, 0x480),
+                                                  # CKPT_OPT_CE_GATHER at m = 2: the copy-engine mirror
+                                                  (2, 4096, 0, 0x10), (2, 65536, 3, 0x10)])
 def test_group_drill_rebuild_every_rank(torch, C, m, unit, n_slots, flags):
     """Failure drill (Q12): rank k loses tensors and host image; rebuild + load."""
     from synth.gpu import fill_state

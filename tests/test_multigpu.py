@@ -216,7 +216,8 @@ def _worker_c2(rank, world, port, q, config="c2_7b_tp8", extra_flags=0):
         q.put((rank, None, traceback.format_exc(), None))
 
 
-@pytest.mark.parametrize("config,flags", [("c2_7b_tp8", 0), ("c4_34b_tp8_stage0", 0), ("c2_7b_tp8", 0x400)])
+@pytest.mark.parametrize("config,flags", [("c2_7b_tp8", 0), ("c4_34b_tp8_stage0", 0), ("c2_7b_tp8", 0x400),
+                                          ("c2_7b_tp8", 0x10)])  # CE gather (m = 2: the CE mirror)
 def test_ipc_full_size_full_image(config, flags):
     """BASELINE configs 2 and 4 at full size in the bench launch configuration (one
     process per GPU, full-copy staging, 512 MiB buckets, TMA pack, TMA XOR over NVLink).
@@ -683,7 +684,8 @@ def test_torchrun_elastic_replaces_a_killed_rank(tmp_path):
     env = dict(os.environ, CKPT_TIMEOUT_S="120")
     try:
         r = subprocess.run(cmd, cwd=root, env=env, capture_output=True, text=True, timeout=600)
-        assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+        errs = "".join(f"--- {f.name}\n{f.read_text()}" for f in sorted(tmp_path.glob("*.err")))
+        assert r.returncode == 0, errs + r.stdout[-2000:] + r.stderr[-3000:]
         res = [json.load(open(tmp_path / f"rank{j}.json")) for j in range(world)]
         for x in res:
             assert x["attempt"] == 1, x       # the group was restarted once by the agent

@@ -91,4 +91,11 @@ def main():
 
 
 if __name__ == "__main__":
-    main()
+    try:
+        main()
+    except BaseException:  # the agent reports only exit codes: keep each attempt's traceback
+        import traceback
+        d = sys.argv[sys.argv.index("--out") + 1]
+        with open(os.path.join(d, f"rank{os.environ.get('RANK')}_attempt{os.environ.get('TORCHELASTIC_RESTART_COUNT')}.err"), "w") as f:
+            f.write(traceback.format_exc())
+        raise

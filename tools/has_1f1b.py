@@ -53,7 +53,10 @@ def main():
     ap.add_argument("--config", default="c3_13b_tp4pp2")
     ap.add_argument("--reps", type=int, default=2)
     ap.add_argument("--out", default="")
+    ap.add_argument("--watchdog-s", type=float, default=600.0)
     a = ap.parse_args()
+
+    import faulthandler
 
     import torch
     import torch.distributed as dist
@@ -62,6 +65,13 @@ def main():
     from synth.gpu import descriptors, make_rank_state
 
     rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
+    if a.watchdog_s > 0:  # a hang dumps every thread's stack and exits instead of burning the call
+        faulthandler.dump_traceback_later(a.watchdog_s, exit=True)
+    t_start = time.time()
+
+    def trace(*x):
+        print(f"[has_1f1b rank {rank} +{time.time() - t_start:7.1f}s]", *x, file=sys.stderr, flush=True)
+
     assert world == 2, "a 2-stage pipeline: run on 2 GPUs"
     local = int(os.environ.get("LOCAL_RANK", rank))
     torch.cuda.set_device(local)
@@ -172,11 +182,13 @@ def main():
     e1.record(s)
     e1.synchronize()
     c_fb_bp = e0.elapsed_time(e1) / 5 / 1e3
+    trace(f"C_FB,BP = {c_fb_bp * 1e3:.2f} ms")
     for _ in range(3):
         timed_iteration()
     dist.barrier()
     base = [timed_iteration() for _ in range(8)]
     base_iter = statistics.median(x["iter_ms"] for x in base)
+    trace(f"baseline iteration {base_iter:.2f} ms")
 
     # ---- snapshot state of this stage -----------------------------------------------
     specs, ts = make_rank_state(a.config, 4 * p, dev)
@@ -214,6 +226,7 @@ def main():
                     raise RuntimeError(f"{name}: snapshot did not complete in 400 iterations")
             C.ckpt_wait(ctx, sid)
             wall = time.perf_counter() - t0
+            trace(f"{name} rep {rep}: committed after {len(its)} iterations, {wall:.2f} s")
             st = C.ckpt_get_stats(ctx)
             during = its[:-1] if len(its) > 1 else its  # the last iteration may end after the commit
             out.append({"iters": len(its),
@@ -234,6 +247,7 @@ def main():
     b_io = S / (ung["snapshot_ms"] / 1e3)
     t_compute = statistics.median(x["pipe_ms"] for x in base) / 1e3 - 0.0  # GEMM phases of one iteration
     plan = C.ckpt_has_plan3(p, P, c_fb_bp, S, b_io, t_compute)
+    trace("plan", plan)
     run_placement("layer1", True, 2 ** 64 - 1, 0)
     run_placement("layers12", True, plan["bubble_bytes"], 2 ** 64 - 1)
     run_placement("layers123", True, plan["bubble_bytes"], plan["compute_bytes"])

@@ -67,7 +67,11 @@ def main():
                       "xor_us": st["xor_ms"] / max(st["xor_launches"], 1) * 1e3,
                       "xor_nvlink_gbs": st["xor_bytes_in"] / max(st["xor_ms"], 1e-9) / 1e6,
                       "pack_hbm_gbs": st["pack_bytes"] / max(st["pack_ms"], 1e-9) / 1e6,
-                      "snapshot_ms": st["last_snapshot_ms"]}))
+                      "snapshot_ms": st["last_snapshot_ms"],
+                      # m = 2 + CKPT_OPT_CE_GATHER: the copy-engine mirror (no XOR kernel)
+                      "ce_mirror_ms": st["gather_ms"] / a.reps if st["gather_ops"] else None,
+                      "ce_mirror_nvlink_gbs": C.ckpt_geometry(ctxs[0])["L_star"] * a.reps / st["gather_ms"] / 1e6
+                      if st["gather_ops"] and st["gather_ms"] > 0 else None}))
     if a.rebuild >= 0:
         k = a.rebuild
         g = C.ckpt_geometry(ctxs[0])
