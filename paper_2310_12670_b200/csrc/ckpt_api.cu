@@ -729,7 +729,7 @@ extern "C" int ckpt_window(ckpt_ctx *c, int open, void *stream) {
     CUresult r = p_write32((CUstream)stream, (CUdeviceptr)(uintptr_t)c->window, (uint32_t)open,
                            CU_STREAM_WRITE_VALUE_DEFAULT);
     if (r != CUDA_SUCCESS) return fail(CKPT_ECUDA, "cuStreamWriteValue32(window) failed (%d)", (int)r);
-    return CKPT_OK;
+    return issue_gated_more(c);  // a pending windowed snapshot: enqueue the next gated copies
 }
 
 extern "C" int ckpt_has_apply(ckpt_ctx *c, uint64_t bubble_bytes) {

@@ -231,6 +231,12 @@ struct ckpt_ctx {
     uint64_t pending_id = 0;   // issued snapshot not yet waited
     bool requested = false;    // LOCAL: ckpt_snapshot called, group not yet issued
     bool issued = false;
+    // HAS windows (CKPT_OPT_WINDOWED, IPC / single member): the window-gated copies are
+    // enqueued progressively, at most kGatedAhead beyond the last completed one, so the
+    // caller's thread never blocks on a full stream queue while the windows it is about to
+    // open are still closed (see issue_gated)
+    uint64_t gate_next = 0, gate_total = 0;
+    bool gate_tail = false;    // stage_finish still to issue
     uint64_t req_bucket = 0;
     uint64_t op_B = 0, op_NB = 0;
     uint32_t op_seq_base = 0;
@@ -380,6 +386,7 @@ void make_sticky(ckpt_ctx *c, int rc);
 void group_abort(ckpt_ctx *c);
 uint32_t peer_aborted(ckpt_ctx *c);
 int host_sync(ckpt_ctx *c);
+int issue_gated_more(ckpt_ctx *c);  // HAS windows: enqueue more window-gated copies
 uint64_t effective_bucket(const ckpt_ctx *c, uint64_t req);
 bool single_launch(const ckpt_ctx *c);
 int issue_pack_all(ckpt_ctx *c);

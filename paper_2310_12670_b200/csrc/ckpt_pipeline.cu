@@ -696,6 +696,59 @@ int begin_member(ckpt_ctx *c, cudaStream_t caller, uint64_t B) {
     return CKPT_OK;
 }
 
+// HAS windows with one process per member: a gated copy waits on the device until the
+// training stream opens its window, and the training stream is driven by the caller's
+// thread -- so if ckpt_snapshot enqueued every bucket at once, a stream queue could fill
+// and block that thread before it opens the first window (observed: a C3 snapshot of 700
+// 32 MiB buckets hung in ckpt_snapshot).  The gated ops (data bucket g < NB; with full-copy
+// staging, parity bucket g - NB after all data) are enqueued at most kGatedAhead beyond
+// the last one whose copy completed; ckpt_window, ckpt_test and ckpt_wait top up.
+constexpr uint64_t kGatedAhead = 32;
+
+bool gated_progressive(const ckpt_ctx *c) {
+    return (c->opt.flags & CKPT_OPT_WINDOWED) && !device_only(c) && !(c->transport == CKPT_GROUP_LOCAL && c->m >= 2);
+}
+
+int issue_gated(ckpt_ctx *c) {
+    int rc;
+    const bool one = single_launch(c);
+    while (c->gate_next < c->gate_total) {
+        if (c->gate_next >= kGatedAhead) {
+            const uint64_t g = c->gate_next - kGatedAhead;
+            cudaEvent_t e = g < c->op_NB ? c->ev_d2h_data[slot_of(c, g)] : c->ev_d2h_par[slot_of(c, g - c->op_NB)];
+            const cudaError_t q = cudaEventQuery(e);
+            if (q == cudaErrorNotReady) return CKPT_OK;
+            if (q != cudaSuccess) return fail(CKPT_ECUDA, "snapshot: %s", cudaGetErrorString(q));
+        }
+        const uint64_t g = c->gate_next;
+        if (g >= c->op_NB) {
+            rc = stage_copy_parity(c, g - c->op_NB);
+        } else if (c->full_copy) {
+            rc = stage_copy(c, g, false);
+        } else {  // ring staging: the whole bucket (its pack waits on an older bucket's copy)
+            if (!one && (rc = stage_pack(c, g))) return rc;
+            if ((rc = stage_xor(c, g)) == CKPT_OK) rc = stage_copy(c, g, true);
+        }
+        if (rc) return rc;
+        ++c->gate_next;
+    }
+    if (c->gate_tail) {
+        if ((rc = stage_finish(c))) return rc;
+        c->gate_tail = false;
+    }
+    return CKPT_OK;
+}
+
+// top-up from the training thread's calls (no-op when nothing is pending)
+int issue_gated_more(ckpt_ctx *c) {
+    if (!c->issued || (c->gate_next >= c->gate_total && !c->gate_tail)) return CKPT_OK;
+    int rc = issue_gated(c);
+    if (rc) make_sticky(c, rc);
+    return rc;
+}
+
+bool gated_pending(const ckpt_ctx *c) { return c->issued && (c->gate_next < c->gate_total || c->gate_tail); }
+
 extern "C" int ckpt_snapshot(ckpt_ctx *c, uint64_t bucket_bytes, void *stream, uint64_t *id) {
     NvtxRange nvtx_("ckpt_snapshot");
     if (!c) return fail(CKPT_EINVAL, "snapshot: null context");
@@ -773,6 +826,31 @@ extern "C" int ckpt_snapshot(ckpt_ctx *c, uint64_t bucket_bytes, void *stream, u
     if (one && (rc = issue_pack_all(c))) {
         make_sticky(c, rc);
         return rc;
+    }
+    if (gated_progressive(c)) {
+        // the un-gated device work first (pack, parity), then the window-gated copies a
+        // few at a time: the rest is issued from ckpt_window / ckpt_test / ckpt_wait
+        for (uint64_t k = 0; c->full_copy && k < c->op_NB; ++k)
+            if ((!one && (rc = stage_pack(c, k))) || (rc = stage_xor(c, k))) {
+                make_sticky(c, rc);
+                return rc;
+            }
+        if (c->full_copy && xor_push(c) && (rc = push_collect(c))) {
+            make_sticky(c, rc);
+            return rc;
+        }
+        c->gate_next = 0;
+        c->gate_total = c->op_NB + (c->full_copy && c->m >= 2 && c->aec ? c->op_NB : 0);
+        c->gate_tail = true;
+        c->pending_id = my_id;
+        c->issued = true;
+        c->st.snapshots++;
+        if ((rc = issue_gated(c))) {
+            make_sticky(c, rc);
+            return rc;
+        }
+        if (id) *id = my_id;
+        return CKPT_OK;
     }
     for (uint64_t k = 0; k < c->op_NB; ++k) {
         if ((!one && (rc = stage_pack(c, k))) || (rc = stage_xor(c, k)) || (rc = stage_copy(c, k, !c->full_copy))) {
@@ -898,6 +976,8 @@ extern "C" int ckpt_test(ckpt_ctx *c, uint64_t id, int *done) {
     if (!c->issued) return CKPT_OK;
     int rc = set_dev(c);
     if (rc) return rc;
+    if ((rc = issue_gated_more(c))) return rc;
+    if (gated_pending(c)) return CKPT_OK;
     auto ready = [](cudaError_t e) { return e == cudaSuccess ? 1 : e == cudaErrorNotReady ? 0 : -1; };
     int r = 1;
     if (c->done_enqueued) {
@@ -925,7 +1005,22 @@ extern "C" int ckpt_wait(ckpt_ctx *c, uint64_t id) {
     if (!c->issued) return fail(CKPT_ESTATE, "wait: LOCAL group snapshot not issued yet (members missing)");
     int rc = set_dev(c);
     if (rc) return rc;
-    rc = wait_done_all(c, c->op_seq_base + (uint32_t)c->op_NB + 1);
+    if (gated_pending(c)) {  // HAS windows: keep topping up until every gated copy is enqueued
+        double limit = 600.0;
+        if (const char *e = getenv("CKPT_TIMEOUT_S")) limit = atof(e);
+        const auto t0 = std::chrono::steady_clock::now();
+        while (!rc && gated_pending(c)) {
+            if ((rc = issue_gated_more(c))) break;
+            if (!gated_pending(c)) break;
+            if (std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count() > limit) {
+                rc = fail(CKPT_EPEER, "wait: window-gated copies made no progress in %.0f s (are the HAS windows "
+                                      "ever opened?)", limit);
+                break;
+            }
+            std::this_thread::sleep_for(std::chrono::microseconds(50));
+        }
+    }
+    if (!rc) rc = wait_done_all(c, c->op_seq_base + (uint32_t)c->op_NB + 1);
     if (!rc) rc = check_sticky(c);
     if (!rc && (c->opt.flags & CKPT_OPT_TIMING)) {
         rc = harvest_timing(c);

@@ -724,6 +724,51 @@ def test_has_window_gates_the_d2h(torch, C):
         C.ckpt_destroy(ctx)
 
 
+@pytest.mark.timeout(300)
+@pytest.mark.parametrize("n_slots", [0, 3])
+def test_has_windowed_snapshot_of_many_buckets_never_blocks_the_caller(torch, C, n_slots):
+    """HAS windows with thousands of buckets (256 MiB in 64 KiB buckets): ckpt_snapshot is
+    issued while every window is closed and must return at once -- the training thread opens
+    the windows only afterwards, so enqueueing every gated copy up front would fill a stream
+    queue and block it forever (the 1F1B run's C3 hang).  The caller then runs a "training
+    loop" of short open/closed window phases (ckpt_window tops up the gated copies) until
+    ckpt_test reports completion; the committed image matches the oracle."""
+    import time
+
+    import synth
+    from synth.gpu import alloc_state, fill_state
+    specs = [synth.TensorSpec(f"t{i}", "fp32" if i % 2 else "bf16", (16 << 20) // (4 if i % 2 else 2) - 3 * i, "param")
+             for i in range(16)]
+    ts = alloc_state(specs, "cuda:0", 1)
+    fill_state(ts, 0)
+    ctx = make_ctx(C, (specs, ts), n_slots=n_slots, bucket_bytes=1 << 16, flags=C.CKPT_OPT_WINDOWED)
+    s = torch.cuda.Stream()
+    try:
+        C.ckpt_protect(ctx, 1, 0)
+        g = C.ckpt_geometry(ctx)
+        assert g["L"] // (1 << 16) >= 4000
+        C.ckpt_window(ctx, 0, s)
+        t0 = time.perf_counter()
+        sid = C.ckpt_snapshot(ctx, 0, s)
+        assert time.perf_counter() - t0 < 20, "ckpt_snapshot blocked while the windows were closed"
+        phases = 0
+        while True:
+            C.ckpt_window(ctx, C.CKPT_WINDOW_COMPUTE, s)
+            torch.cuda._sleep(2_000_000)          # ~1 ms of "computation" with the window open
+            C.ckpt_window(ctx, 0, s)
+            torch.cuda._sleep(1_000_000)          # an HBM-bound phase: closed
+            s.synchronize()
+            phases += 1
+            if C.ckpt_test(ctx, sid):
+                break
+            assert phases < 20000, "the windowed snapshot made no progress"
+        C.ckpt_wait(ctx, sid)
+        want, _, _ = oracle_image(specs, 0, g["L_star"])
+        assert_bytes_equal(C.ckpt_host_view(ctx, 0, copy=True)[0], want, "windowed image of 4096 buckets")
+    finally:
+        C.ckpt_destroy(ctx)
+
+
 def test_has_split_places_buckets_in_their_windows(torch, C):
     """Alg 1 SplitParameter in the scheduler (ckpt_has_apply): the first bubble_bytes of the
     image go out only in CKPT_WINDOW_BUBBLE windows (they lead, so a compute window moves

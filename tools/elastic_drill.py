@@ -45,7 +45,15 @@ def main():
     lost = world - 1
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    dist.init_process_group("nccl", device_id=dev)
+    # torchrun's static rendezvous (--master-addr/--master-port) keeps ONE agent store across
+    # restarts and gives the workers no per-attempt prefix, so a restarted group would read
+    # attempt 0's NCCL bootstrap keys (a dead rank 0's address): prefix them by attempt
+    from datetime import timedelta
+    agent_store = os.environ.get("TORCHELASTIC_USE_AGENT_STORE") == "True"
+    base = dist.TCPStore(os.environ["MASTER_ADDR"], int(os.environ["MASTER_PORT"]), world,
+                         is_master=(not agent_store and rank == 0), timeout=timedelta(seconds=300))
+    store = dist.PrefixStore(f"/reft-elastic-drill/attempt{attempt}", base)
+    dist.init_process_group("nccl", store=store, rank=rank, world_size=world, device_id=dev)
     specs = synth.config_tensors(a.config, rank)
     ts = alloc_state(specs, dev, misalign=1)
     o = C.ckpt_options_default(n_slots=0, bucket_bytes=1 << 16, stripe_unit=4096, flags=C.CKPT_OPT_SHM_ARENA,
