@@ -605,10 +605,12 @@ def registered_host_buffer(torch, n):
     return _Registered(torch, n)
 
 
-def gemm_corun(torch, C, ctx, stream, bucket, barrier, allmax, dev, pairs=10):
+def gemm_corun(torch, C, ctx, stream, bucket, barrier, allmax, dev, pairs=12):
     """bf16 8192^3 GEMMs back to back on a HIGH-priority stream; slowdown while a snapshot
     runs on the library's low-priority streams (the O_in-mem analog, P.234-236; HAS Layer 2,
-    P.423).  `pairs` interleaved A/B windows (alone, with snapshot), each >= 1.5x a snapshot.
+    P.423).  `pairs` interleaved pairs of windows (alone, with snapshot) in ABBA order, each >= 2x a
+    snapshot; the with-snapshot windows also give an in-window slowdown against their own
+    GEMMs after the commit.
     Every GEMM is bracketed by its own CUDA events, so besides the whole window the slowdown
     is also reported over the GEMMs that overlap the pack kernel (the pack window) and the
     device-side protect (pack + XOR), located relative to an event recorded on the caller
@@ -632,7 +634,7 @@ def gemm_corun(torch, C, ctx, stream, bucket, barrier, allmax, dev, pairs=10):
     sid = C.ckpt_snapshot(ctx, bucket, stream)
     C.ckpt_wait(ctx, sid)
     snap_ms = C.ckpt_get_stats(ctx)["last_snapshot_ms"] or 250.0
-    iters = int(allmax(int(max(20, 1.5 * snap_ms / per))))
+    iters = int(allmax(int(max(20, 2.0 * snap_ms / per))))
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(iters)]
 
     def window(with_snap):
@@ -666,14 +668,24 @@ def gemm_corun(torch, C, ctx, stream, bucket, barrier, allmax, dev, pairs=10):
         return (sum(d) / len(d), len(d)) if d else (None, 0)
 
     rows = []
-    for _ in range(pairs):
-        ta, sa, _, _, _ = window(False)
-        tw, sw, pack, xor, snap = window(True)
+    for i in range(pairs):
+        # ABBA order: the GEMM slows as the GPU warms up, so alternate which window runs first
+        if i % 2 == 0:
+            ta, sa, _, _, _ = window(False)
+            tw, sw, pack, xor, snap = window(True)
+        else:
+            tw, sw, pack, xor, snap = window(True)
+            ta, sa, _, _, _ = window(False)
         base = sum(b - a for a, b in sa[2:]) / max(1, len(sa) - 2)  # per-GEMM time alone (warm)
         pw, npw = overlap_mean(sw, 0.0, pack)
         dw, ndw = overlap_mean(sw, 0.0, pack + xor)
         sn, nsn = overlap_mean(sw, 0.0, snap or 0.0)
+        # in-window baseline: the same window's GEMMs that start after the snapshot committed
+        # (same clocks and temperature as the overlapped ones)
+        tail = [b - a for a, b in sw if snap and a > snap + 1.0]
+        tl = sum(tail) / len(tail) if len(tail) >= 5 else None
         rows.append({"whole_pct": (tw / ta - 1) * 100,
+                     "in_window_pct": (sn / tl - 1) * 100 if sn and tl else None, "tail_gemms": len(tail),
                      "pack_window_pct": (pw / base - 1) * 100 if pw else None, "pack_window_gemms": npw,
                      "protect_window_pct": (dw / base - 1) * 100 if dw else None,
                      "snapshot_window_pct": (sn / base - 1) * 100 if sn else None,
@@ -688,13 +700,14 @@ def gemm_corun(torch, C, ctx, stream, bucket, barrier, allmax, dev, pairs=10):
 
     flops = 2 * n ** 3 * iters
     whole = summ("whole_pct")
-    return {"slowdown_pct": whole["median"], "whole_window": whole,
+    return {"slowdown_pct": whole["median"], "whole_window": whole, "in_window": summ("in_window_pct"),
             "pack_window": summ("pack_window_pct"), "protect_window": summ("protect_window_pct"),
             "snapshot_window": summ("snapshot_window_pct"),
             "pairs": [{k: (round(v, 3) if isinstance(v, float) else v) for k, v in r.items()} for r in rows],
             "gemm_iters": iters, "gemm_tflops_alone": round(flops / statistics.median([r["alone_ms"] for r in rows]) / 1e9, 1),
             "snapshot_ms_alone": round(snap_ms, 3),
-            "window": (f"{pairs} interleaved A/B pairs; whole = GEMM window (>= 1.5x snapshot, max over ranks); "
+            "window": (f"{pairs} interleaved pairs in ABBA order; whole = GEMM window (>= 2x snapshot, max over ranks); "
+                       "in_window = GEMMs overlapping the snapshot vs the same window's GEMMs after its commit; "
                        "pack / protect / snapshot window = mean per-GEMM time of the GEMMs overlapping "
                        "[capture, +pack] / [capture, +pack+xor] / [capture, +snapshot] vs the warm per-GEMM "
                        "time alone (this rank)")}

@@ -85,8 +85,13 @@ extern "C" {
 #define CKPT_OPT_REBUILD_SHARES 0x200u /* rebuild: the m-1 survivors each encode 1/(m-1) of
                                       the lost member's parity row into its parity buffer
                                       (reading Q27): the lost GPU receives L*.m/(m-1) instead
-                                      of 2.L* over NVLink.  Every member must agree (else
-                                      ckpt_protect returns EMISMATCH)                      */
+                                      of 2.L* over NVLink.  The DEFAULT for m >= 3 (measured
+                                      C5 m = 4: 54.5 vs 70.7 ms); this flag forces it at m = 2
+                                      too.  Every member must agree (else ckpt_protect
+                                      returns EMISMATCH)                                   */
+#define CKPT_OPT_REBUILD_SELF 0x800u /* rebuild: the lost member re-encodes its own parity
+                                      row from the survivors' data (2.L* into the lost GPU;
+                                      the default at m = 2).  Must agree like the above     */
 #define CKPT_OPT_XOR_PUSH    0x400u /* parity encode in push mode (full-copy staging only;
                                       otherwise ignored): every member sends each unit of its
                                       own image to its row owner as a bulk XOR reduction

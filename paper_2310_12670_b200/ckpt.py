@@ -39,6 +39,7 @@ CKPT_OPT_SHM_ARENA = 0x40
 CKPT_OPT_HOST_LOAD = 0x80
 CKPT_OPT_WINDOWED = 0x100
 CKPT_OPT_REBUILD_SHARES = 0x200
+CKPT_OPT_REBUILD_SELF = 0x800
 CKPT_OPT_XOR_PUSH = 0x400
 CKPT_PROBE_SM_PULL, CKPT_PROBE_CE_PULL = 0, 1
 CKPT_SCHEME_DEFAULT, CKPT_SCHEME_AEC, CKPT_SCHEME_ARC, CKPT_SCHEME_ARC_AEC = 0, 1, 2, 3

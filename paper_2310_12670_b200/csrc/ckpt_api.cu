@@ -596,8 +596,8 @@ extern "C" int ckpt_protect(ckpt_ctx *c, const ckpt_group *g) {
         for (uint32_t j = 0; j < m; ++j) {
             if (hb[j]->arena_key != c->opt.arena_key)
                 return fail(CKPT_EMISMATCH, "protect: member %u uses another arena key", j);
-            if ((hb[j]->opt_flags ^ c->opt.flags) & (CKPT_OPT_REBUILD_SHARES | CKPT_OPT_XOR_PUSH))
-                return fail(CKPT_EMISMATCH, "protect: members disagree on CKPT_OPT_REBUILD_SHARES / CKPT_OPT_XOR_PUSH (member %u)", j);
+            if ((hb[j]->opt_flags ^ c->opt.flags) & (CKPT_OPT_REBUILD_SHARES | CKPT_OPT_REBUILD_SELF | CKPT_OPT_XOR_PUSH))
+                return fail(CKPT_EMISMATCH, "protect: members disagree on CKPT_OPT_REBUILD_SHARES / _SELF / CKPT_OPT_XOR_PUSH (member %u)", j);
             c->group_version = std::max(c->group_version, hb[j]->attached_id);
         }
         for (uint32_t j = 0; j < m; ++j) {
@@ -637,8 +637,8 @@ extern "C" int ckpt_protect(ckpt_ctx *c, const ckpt_group *g) {
             if (!g->members[j]) return fail(CKPT_EINVAL, "protect: LOCAL group member %u is NULL", j);
             if (g->members[j]->opt.arena_key != c->opt.arena_key)
                 return fail(CKPT_EMISMATCH, "protect: member %u uses another arena key", j);
-            if ((g->members[j]->opt.flags ^ c->opt.flags) & (CKPT_OPT_REBUILD_SHARES | CKPT_OPT_XOR_PUSH))
-                return fail(CKPT_EMISMATCH, "protect: members disagree on CKPT_OPT_REBUILD_SHARES / CKPT_OPT_XOR_PUSH (member %u)", j);
+            if ((g->members[j]->opt.flags ^ c->opt.flags) & (CKPT_OPT_REBUILD_SHARES | CKPT_OPT_REBUILD_SELF | CKPT_OPT_XOR_PUSH))
+                return fail(CKPT_EMISMATCH, "protect: members disagree on CKPT_OPT_REBUILD_SHARES / _SELF / CKPT_OPT_XOR_PUSH (member %u)", j);
             c->group_version = std::max(c->group_version, g->members[j]->attached_id);
         }
         for (uint32_t j = 0; j < m; ++j) {

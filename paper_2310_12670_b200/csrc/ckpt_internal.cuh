@@ -377,9 +377,15 @@ int rebuild_map_parity(ckpt_ctx *c, uint32_t kl, bool wait = false);
 bool xor_push(const ckpt_ctx *c);
 int push_issue(ckpt_ctx *c);
 int push_collect(ckpt_ctx *c);
-// Without CKPT_OPT_REBUILD_SHARES the lost member re-encodes its own parity row (pulling
-// L* more over NVLink); with it the survivors encode it in shares (Q27)
-static inline bool rebuild_self_encode(const ckpt_ctx *c) { return !(c->opt.flags & CKPT_OPT_REBUILD_SHARES); }
+// Who re-encodes the lost member's parity row (Q27): the survivors in shares (the default
+// for m >= 3, forced at any m by CKPT_OPT_REBUILD_SHARES) or the lost member itself,
+// pulling L* more over NVLink (the default at m = 2, forced by CKPT_OPT_REBUILD_SELF).
+// Round-2 A/B (tools/rb_share_ab.sh): C5 m = 4 54.5 / 55.0 ms in shares vs 70.7 / 70.4 ms
+// self; C2 m = 2 35.6 / 34.6 ms vs 32.8 / 32.9 ms.
+static inline bool rebuild_self_encode(const ckpt_ctx *c) {
+    if (c->opt.flags & CKPT_OPT_REBUILD_SELF) return true;
+    return !(c->opt.flags & CKPT_OPT_REBUILD_SHARES) && c->m <= 2;
+}
 void clean_pad(ckpt_ctx *c, int buf);
 int check_sticky(ckpt_ctx *c);
 void make_sticky(ckpt_ctx *c, int rc);

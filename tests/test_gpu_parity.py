@@ -118,11 +118,12 @@ def make_group(torch, C, m, unit, n_slots=0, bucket=1 << 20, flags=0, misalign=0
     return states, ctxs
 
 
-def test_rebuild_shares_flag_must_agree(torch, C):
-    """CKPT_OPT_REBUILD_SHARES changes who writes the lost member's parity row (Q27): a
-    group whose members disagree would leave it unwritten or written twice -> EMISMATCH."""
+@pytest.mark.parametrize("flag", [0x200, 0x800])
+def test_rebuild_shares_flag_must_agree(torch, C, flag):
+    """CKPT_OPT_REBUILD_SHARES / _SELF change who writes the lost member's parity row (Q27):
+    a group whose members disagree would leave it unwritten or written twice -> EMISMATCH."""
     states = [tiny(j) for j in range(3)]
-    ctxs = [make_ctx(C, st, n_slots=0, bucket_bytes=1 << 20, flags=C.CKPT_OPT_REBUILD_SHARES if j == 1 else 0)
+    ctxs = [make_ctx(C, st, n_slots=0, bucket_bytes=1 << 20, flags=flag if j == 1 else 0)
             for j, st in enumerate(states)]
     try:
         with pytest.raises(C.CkptError) as e:
@@ -219,7 +220,10 @@ def test_group_encode_matches_oracle(torch, C, m, unit, n_slots, bucket, flags):
                                                   (2, 4096, 0, 0x400), (4, 65536, 0, 0x402), (8, 1024, 0, 0x600),
                                                   (5, 16, 0, 0x480),
                                                   # CKPT_OPT_CE_GATHER at m = 2: the copy-engine mirror
-                                                  (2, 4096, 0, 0x10), (2, 65536, 3, 0x10)])
+                                                  (2, 4096, 0, 0x10), (2, 65536, 3, 0x10),
+                                                  # CKPT_OPT_REBUILD_SELF at m >= 3 (the default there is shares)
+                                                  (4, 4096, 2, 0x800), (5, 65536, 0, 0x802), (3, 4096, 0, 0x880),
+                                                  (8, 1024, 0, 0x800)])
 def test_group_drill_rebuild_every_rank(torch, C, m, unit, n_slots, flags):
     """Failure drill (Q12): rank k loses tensors and host image; rebuild + load."""
     from synth.gpu import fill_state

@@ -137,6 +137,7 @@ def _world():
     ("tiny_5", 256, 0, 1 << 20, 0x10, 0),
     ("tiny_7", 4096, 0, 1 << 20, 0x200, 1),  # CKPT_OPT_REBUILD_SHARES (Q27)
     ("tiny_5", 1024, 2, 1 << 16, 0x200, 0),
+    ("tiny_5", 4096, 0, 1 << 16, 0x800, 1),  # CKPT_OPT_REBUILD_SELF (the default at m >= 3 is shares)
     ("tiny_7", 4096, 0, 1 << 20, 0x400, 1),  # CKPT_OPT_XOR_PUSH: bulk XOR reductions over NVLink
     ("tiny_6", 16, 0, 1 << 16, 0x600, 0),
 ])

@@ -22,6 +22,7 @@ def main():
     p.add_argument("--reps", type=int, default=3)
     p.add_argument("--bucket", type=int, default=64 << 20)
     p.add_argument("--flags", type=int, default=0)
+    p.add_argument("--unit", type=int, default=65536, help="stripe unit u (Q4)")
     p.add_argument("--with-d2h", action="store_true", help="run a pinned D2H on every device meanwhile")
     p.add_argument("--rebuild", type=int, default=-1,
                    help="then lose member k (device copy + host image) and rebuild it from the survivors' "
@@ -37,7 +38,7 @@ def main():
     for j in range(m):
         torch.cuda.set_device(j)
         specs, ts = make_rank_state(a.config, j, torch.device("cuda", j))
-        c = C.ckpt_create(j, C.ckpt_options_default(n_slots=0, bucket_bytes=a.bucket,
+        c = C.ckpt_create(j, C.ckpt_options_default(n_slots=0, bucket_bytes=a.bucket, stripe_unit=a.unit,
                                                     flags=C.CKPT_OPT_TIMING | C.CKPT_OPT_DEVICE_ONLY | a.flags))
         C.ckpt_register(c, descriptors(ts, specs))
         ctxs.append(c)
@@ -63,7 +64,7 @@ def main():
         for c, i in zip(ctxs, ids):
             C.ckpt_wait(c, i)
     st = C.ckpt_get_stats(ctxs[0])
-    print(json.dumps({"m": m, "config": a.config, "pack_us": st["pack_ms"] / max(st["pack_launches"], 1) * 1e3,
+    print(json.dumps({"m": m, "config": a.config, "unit": C.ckpt_geometry(ctxs[0])["unit"], "pack_us": st["pack_ms"] / max(st["pack_launches"], 1) * 1e3,
                       "xor_us": st["xor_ms"] / max(st["xor_launches"], 1) * 1e3,
                       "xor_nvlink_gbs": st["xor_bytes_in"] / max(st["xor_ms"], 1e-9) / 1e6,
                       "pack_hbm_gbs": st["pack_bytes"] / max(st["pack_ms"], 1e-9) / 1e6,
