@@ -206,6 +206,17 @@ extern "C" int ckpt_destroy(ckpt_ctx *c) {
     for (auto &t : c->host_bg)  // background host copies of an ARC restore
         if (t.joinable()) t.join();
     cudaSetDevice(c->device);
+    if (c->window && (c->opt.flags & CKPT_OPT_WINDOWED)) {
+        // a snapshot still waiting for a HAS window the caller will never open: open every
+        // window so the copy stream drains (the gated copies not yet enqueued are dropped)
+        cudaStream_t t = nullptr;
+        if (cudaStreamCreateWithFlags(&t, cudaStreamNonBlocking) == cudaSuccess) {
+            cudaMemsetAsync(c->window, 0xff, sizeof(uint32_t), t);
+            cudaStreamSynchronize(t);
+            cudaStreamDestroy(t);
+        }
+        cudaGetLastError();
+    }
     cudaStream_t ss[5] = {c->sP, c->sX, c->sC, c->sW, c->sG};
     for (auto s : ss)
         if (s) cudaStreamSynchronize(s);

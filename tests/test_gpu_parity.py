@@ -755,9 +755,9 @@ def test_has_windowed_snapshot_of_many_buckets_never_blocks_the_caller(torch, C,
         t0 = time.perf_counter()
         sid = C.ckpt_snapshot(ctx, 0, s)
         assert time.perf_counter() - t0 < 20, "ckpt_snapshot blocked while the windows were closed"
-        phases = 0
+        phases, t1 = 0, time.perf_counter()
         while True:
-            C.ckpt_window(ctx, C.CKPT_WINDOW_COMPUTE, s)
+            C.ckpt_window(ctx, C.CKPT_WINDOW_BUBBLE | C.CKPT_WINDOW_COMPUTE, s)
             torch.cuda._sleep(2_000_000)          # ~1 ms of "computation" with the window open
             C.ckpt_window(ctx, 0, s)
             torch.cuda._sleep(1_000_000)          # an HBM-bound phase: closed
@@ -765,7 +765,7 @@ def test_has_windowed_snapshot_of_many_buckets_never_blocks_the_caller(torch, C,
             phases += 1
             if C.ckpt_test(ctx, sid):
                 break
-            assert phases < 20000, "the windowed snapshot made no progress"
+            assert time.perf_counter() - t1 < 60, f"the windowed snapshot made no progress ({phases} phases)"
         C.ckpt_wait(ctx, sid)
         want, _, _ = oracle_image(specs, 0, g["L_star"])
         assert_bytes_equal(C.ckpt_host_view(ctx, 0, copy=True)[0], want, "windowed image of 4096 buckets")
