@@ -107,6 +107,60 @@ class Clocks:
                 "reasons": reasons, "samples": len(rows)}
 
 
+class NvmlSampler:
+    """SM clock, power and clock-event reasons of one GPU every few ms on a host thread
+    (NVML), between start() and stop(): the co-run windows are ~0.4 s, too short for the
+    nvidia-smi loop.  stop() -> {"sm_mhz": mean, "power_w": mean, "power_cap": bool}."""
+
+    def __init__(self, torch, dev, period_s: float = 0.005):
+        self.ok = False
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            p = torch.cuda.get_device_properties(dev)  # the same GPU whatever CUDA_VISIBLE_DEVICES says
+            try:
+                self.h = pynvml.nvmlDeviceGetHandleByPciBusId(f"{p.pci_domain_id:08X}:{p.pci_bus_id:02X}:{p.pci_device_id:02X}.0")
+            except Exception:
+                self.h = pynvml.nvmlDeviceGetHandleByIndex(dev.index or 0)
+            self.ok = True
+        except Exception:
+            pass
+        self.period = period_s
+
+    def start(self):
+        import threading
+        self.samples, self.run = [], True
+        if not self.ok:
+            return
+
+        def loop():
+            nv, h = self.nv, self.h
+            while self.run:
+                try:
+                    self.samples.append((nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM),
+                                         nv.nvmlDeviceGetPowerUsage(h) / 1000.0,
+                                         nv.nvmlDeviceGetCurrentClocksEventReasons(h)))
+                except Exception:
+                    pass
+                time.sleep(self.period)
+        self.t = threading.Thread(target=loop, daemon=True)
+        self.t.start()
+
+    def stop(self):
+        self.run = False
+        if not self.ok:
+            return None
+        self.t.join()
+        if not self.samples:
+            return None
+        cap = self.nv.nvmlClocksEventReasonSwPowerCap
+        return {"sm_mhz": statistics.mean(x[0] for x in self.samples),
+                "power_w": statistics.mean(x[1] for x in self.samples),
+                "power_cap_frac": sum(1 for x in self.samples if x[2] & cap) / len(self.samples),
+                "samples": len(self.samples)}
+
+
 # ------------------------------------------------------------------ CPU oracle ------
 class OracleGroup:
     """The unchanged oracle on `threads` host threads at once for an m-member group: thread i
@@ -637,9 +691,12 @@ def gemm_corun(torch, C, ctx, stream, bucket, barrier, allmax, dev, pairs=12):
     iters = int(allmax(int(max(20, 2.0 * snap_ms / per))))
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(iters)]
 
+    nvml = NvmlSampler(torch, dev)
+
     def window(with_snap):
         barrier()
         torch.cuda.synchronize()
+        nvml.start()
         es = torch.cuda.Event(enable_timing=True)
         sid = None
         st0 = C.ckpt_get_stats(ctx)
@@ -654,6 +711,7 @@ def gemm_corun(torch, C, ctx, stream, bucket, barrier, allmax, dev, pairs=12):
         if sid is not None:
             C.ckpt_wait(ctx, sid)
         ev[-1][1].synchronize()
+        clk.append(nvml.stop())
         st1 = C.ckpt_get_stats(ctx)
         total = ev[0][0].elapsed_time(ev[-1][1])
         spans = [(es.elapsed_time(g0), es.elapsed_time(g1)) for g0, g1 in ev]
@@ -667,7 +725,7 @@ def gemm_corun(torch, C, ctx, stream, bucket, barrier, allmax, dev, pairs=12):
         d = [b - a for a, b in spans if b > lo and a < hi_]
         return (sum(d) / len(d), len(d)) if d else (None, 0)
 
-    rows = []
+    rows, clk = [], []
     for i in range(pairs):
         # ABBA order: the GEMM slows as the GPU warms up, so alternate which window runs first
         if i % 2 == 0:
@@ -684,7 +742,13 @@ def gemm_corun(torch, C, ctx, stream, bucket, barrier, allmax, dev, pairs=12):
         # (same clocks and temperature as the overlapped ones)
         tail = [b - a for a, b in sw if snap and a > snap + 1.0]
         tl = sum(tail) / len(tail) if len(tail) >= 5 else None
-        rows.append({"whole_pct": (tw / ta - 1) * 100,
+        ca, cw = (clk[-2], clk[-1]) if i % 2 == 0 else (clk[-1], clk[-2])
+        rows.append({"sm_mhz_alone": ca and round(ca["sm_mhz"], 1), "sm_mhz_with": cw and round(cw["sm_mhz"], 1),
+                     "power_w_alone": ca and round(ca["power_w"], 1), "power_w_with": cw and round(cw["power_w"], 1),
+                     "power_cap_frac_alone": ca and round(ca["power_cap_frac"], 3),
+                     "power_cap_frac_with": cw and round(cw["power_cap_frac"], 3),
+                     "clock_drop_pct": (ca["sm_mhz"] / cw["sm_mhz"] - 1) * 100 if ca and cw else None,
+                     "whole_pct": (tw / ta - 1) * 100,
                      "in_window_pct": (sn / tl - 1) * 100 if sn and tl else None, "tail_gemms": len(tail),
                      "pack_window_pct": (pw / base - 1) * 100 if pw else None, "pack_window_gemms": npw,
                      "protect_window_pct": (dw / base - 1) * 100 if dw else None,
@@ -701,6 +765,10 @@ def gemm_corun(torch, C, ctx, stream, bucket, barrier, allmax, dev, pairs=12):
     flops = 2 * n ** 3 * iters
     whole = summ("whole_pct")
     return {"slowdown_pct": whole["median"], "whole_window": whole, "in_window": summ("in_window_pct"),
+            "clock_drop_pct": summ("clock_drop_pct"),
+            "sm_mhz": {"alone": summ("sm_mhz_alone"), "with": summ("sm_mhz_with")},
+            "power_w": {"alone": summ("power_w_alone"), "with": summ("power_w_with")},
+            "power_cap_frac": {"alone": summ("power_cap_frac_alone"), "with": summ("power_cap_frac_with")},
             "pack_window": summ("pack_window_pct"), "protect_window": summ("protect_window_pct"),
             "snapshot_window": summ("snapshot_window_pct"),
             "pairs": [{k: (round(v, 3) if isinstance(v, float) else v) for k, v in r.items()} for r in rows],

@@ -269,7 +269,11 @@ int ckpt_protect(ckpt_ctx *ctx, const ckpt_group *g);
 int ckpt_snapshot(ckpt_ctx *ctx, uint64_t bucket_bytes, void *stream, uint64_t *id);
 
 /* Make `stream` wait until snapshot `id` no longer reads the registered tensors
- * (all buckets packed) -- call before the next optimizer step mutates them. */
+ * (all buckets packed) -- call before the next optimizer step mutates them.
+ * With CKPT_OPT_WINDOWED and ring staging (n_slots > 0) the packs of later buckets are
+ * enqueued only as earlier buckets reach host memory inside the HAS windows (their ring
+ * slots are reused), so until every pack is issued this returns EBUSY: keep opening
+ * windows (ckpt_window) and call ckpt_test / ckpt_wait, or use full-copy staging. */
 int ckpt_fence(ckpt_ctx *ctx, uint64_t id, void *stream);
 
 /* Host-block until snapshot `id`'s data and parity have landed in host memory on

@@ -835,6 +835,7 @@ extern "C" int ckpt_snapshot(ckpt_ctx *c, uint64_t bucket_bytes, void *stream, u
                 make_sticky(c, rc);
                 return rc;
             }
+        if (c->full_copy && !one) CUDA_TRY(cudaEventRecord(c->ev_pack_all, c->sP));  // every pack issued: ckpt_fence
         if (c->full_copy && xor_push(c) && (rc = push_collect(c))) {
             make_sticky(c, rc);
             return rc;
@@ -886,6 +887,10 @@ extern "C" int ckpt_fence(ckpt_ctx *c, uint64_t id, void *stream) {
     if (!c->issued) return fail(CKPT_ESTATE, "fence: LOCAL group snapshot not issued yet (members missing)");
     int rc = set_dev(c);
     if (rc) return rc;
+    if (!c->full_copy && gated_pending(c) && (rc = issue_gated_more(c))) return rc;
+    if (!c->full_copy && gated_pending(c))
+        return fail(CKPT_EBUSY, "fence: windowed ring snapshot %llu still issuing its packs (open the HAS windows, "
+                                "then ckpt_test / ckpt_wait)", (unsigned long long)id);
     CUDA_TRY(cudaStreamWaitEvent((cudaStream_t)stream, c->ev_pack_all, 0));
     return CKPT_OK;
 }

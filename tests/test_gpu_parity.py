@@ -755,6 +755,12 @@ def test_has_windowed_snapshot_of_many_buckets_never_blocks_the_caller(torch, C,
         t0 = time.perf_counter()
         sid = C.ckpt_snapshot(ctx, 0, s)
         assert time.perf_counter() - t0 < 20, "ckpt_snapshot blocked while the windows were closed"
+        if n_slots:  # ring: later packs wait for earlier buckets' D2H, so the fence cannot be placed yet
+            with pytest.raises(C.CkptError) as e:
+                C.ckpt_fence(ctx, sid, s)
+            assert e.value.code == C.CKPT_EBUSY
+        else:        # full copy: every pack is already enqueued
+            C.ckpt_fence(ctx, sid, s)
         phases, t1 = 0, time.perf_counter()
         while True:
             C.ckpt_window(ctx, C.CKPT_WINDOW_BUBBLE | C.CKPT_WINDOW_COMPUTE, s)
