@@ -107,7 +107,8 @@ def main():
             import bench
             co = bench.gemm_corun(torch, C, ctx, st0, bmib << 20, bar, amax, dev)
             rec["gemm_slowdown_pct"] = co["slowdown_pct"]
-            rec["gemm_corun"] = {k: co[k] for k in ("whole_window", "pack_window", "protect_window", "snapshot_window")}
+            rec["gemm_corun"] = {k: co[k] for k in ("whole_window", "in_window", "pack_window", "protect_window",
+                                                    "snapshot_window", "clock_drop_pct", "sm_mhz", "power_w")}
         if a.drill and g["m"] >= 2:
             lost = [tuple(int(y) for y in x.split("+")) for x in a.lost.split(",")] if a.lost else [(0,), (g["m"] - 1,)]
             C.ckpt_stats_reset(ctx)
