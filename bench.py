@@ -39,7 +39,7 @@ def parse():
     p.add_argument("--config", default="c2_7b_tp8")
     p.add_argument("--bucket", type=int, default=512 << 20)
     p.add_argument("--n-slots", type=int, default=0, help="0 = full device copy (single-launch pack)")
-    p.add_argument("--unit", type=int, default=64 << 10)
+    p.add_argument("--unit", type=int, default=1 << 20, help="stripe unit u (Q4; 1 MiB: DESIGN 11b)")
     p.add_argument("--pack", default="tma", choices=["lsu", "tma", "ce"],
                    help="pack kernel: 128-bit LSU, TMA bulk through SMEM, or copy engines (zero SMs)")
     p.add_argument("--gather", default="kernel", choices=["kernel", "ce"],
@@ -169,13 +169,13 @@ class OracleGroup:
     pack (O3) of every member, the parity of every row (O4) and the rebuild of member 0
     (O6) on it.  Inputs are generated once, before any clock starts; run() times one pass."""
 
-    def __init__(self, config: str, m: int, seconds: float, threads: int):
+    def __init__(self, config: str, m: int, seconds: float, threads: int, unit: int = 1 << 20):
         import bisect
 
         import oracle
         import synth
 
-        self.oracle, self.m, self.threads, self.u, self.config = oracle, m, threads, 65536, config
+        self.oracle, self.m, self.threads, self.u, self.config = oracle, m, threads, unit, config
         stripe = (m - 1) * self.u if m > 1 else 65536
         specs = [synth.config_tensors(config, j) for j in range(m)]
         nb = [[s_.nbytes for s_ in sp] for sp in specs]
@@ -222,7 +222,7 @@ class OracleGroup:
         return time.perf_counter() - t0
 
 
-def oracle_sample(config: str, m: int, seconds: float, step_seed: int = 0):
+def oracle_sample(config: str, m: int, seconds: float, step_seed: int = 0, unit: int = 1 << 20):
     """Time the CPU oracle (as it stands) on a bounded sample of the workload: the first
     tensors of each of the m ranks (up to a byte budget sized for ~`seconds` of work),
     pack (O3) and, for m >= 2, the parity of every rank (O4).  Returns (GB/s of state,
@@ -247,7 +247,7 @@ def oracle_sample(config: str, m: int, seconds: float, step_seed: int = 0):
             imgs.append((ts, off, L))
             tot += acc
         Ls = max(x[2] for x in imgs)
-        Lstar, u = oracle.common_length([x[2] for x in imgs], 65536) if m > 1 else (Ls, 65536)
+        Lstar, u = oracle.common_length([x[2] for x in imgs], unit) if m > 1 else (Ls, unit)
         t0 = time.perf_counter()
         Ds = [oracle.pack(ts, off, Lstar) for ts, off, _ in imgs]
         if m > 1:
@@ -275,7 +275,7 @@ def reference_arm(a, rank, world):
         return 0
     m = max(world, a.gpus)
     nthr = os.cpu_count() or 1
-    og = OracleGroup(a.config, m, max(a.cpu_seconds / max(a.steps, 1), 1.0), nthr)
+    og = OracleGroup(a.config, m, max(a.cpu_seconds / max(a.steps, 1), 1.0), nthr, a.unit)
     for _ in range(a.warmup):
         og.run()
     t_all = sum(og.run() for _ in range(a.steps))
@@ -579,16 +579,16 @@ def main():
 
     cpu = None
     if rank == 0 and world == 1 and not a.no_cpu_baseline:
-        gbs, desc, _, _ = oracle_sample(a.config, 1, a.cpu_seconds)
+        gbs, desc, _, _ = oracle_sample(a.config, 1, a.cpu_seconds, unit=a.unit)
         cpu = {"value": round(gbs, 4), "unit": "GB/s", "cores": 1, "kind": "oracle", "sample": desc}
         nthr = os.cpu_count() or 1
-        og = OracleGroup(a.config, 1, min(a.cpu_seconds, 8.0), nthr)
+        og = OracleGroup(a.config, 1, min(a.cpu_seconds, 8.0), nthr, a.unit)
         dt = og.run()
         cpu["all_cores"] = {"value": round(og.state_bytes / dt / 1e9, 4), "unit": "GB/s", "cores": nthr,
                             "kind": "oracle", "sample": og.desc}
         # the oracle's encode and rebuild (O4, O6) on all cores for a 4-member group: the
         # host-side counterpart of the parity work a protected N >= 2 step does
-        og = OracleGroup(a.config, 4, min(a.cpu_seconds, 8.0), nthr)
+        og = OracleGroup(a.config, 4, min(a.cpu_seconds, 8.0), nthr, a.unit)
         dt = og.run()
         cpu["parity_all_cores_m4"] = {"value": round(og.state_bytes / dt / 1e9 / 4, 4),
                                       "unit": "GB/s per member", "group_gbs": round(og.state_bytes / dt / 1e9, 4),

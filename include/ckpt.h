@@ -108,8 +108,12 @@ typedef struct ckpt_options {
     uint32_t struct_size;   /* sizeof(ckpt_options); set by ckpt_options_default       */
     uint32_t align;         /* A: packed segment alignment, power of 2 in [16, 4096];
                                default 256 (reading Q6)                                  */
-    uint64_t stripe_unit;   /* u: bytes, multiple of 16; default 65536 (Q4);
-                               0 = one stripe, u = L* /(m-1) (SPEC S.378)                 */
+    uint64_t stripe_unit;   /* u: bytes, multiple of 16; default 1 MiB (Q4: at m = 4 the
+                               encode's strided peer reads run at 612 GB/s with 16-64 KiB
+                               units and at the all-to-all pull rate, 672, from 1 MiB);
+                               0 = one stripe, u = L* /(m-1) (SPEC S.378).  The image is
+                               padded to whole stripes ((m-1)u): small shards want a
+                               smaller u                                                 */
     uint64_t bucket_bytes;  /* ring slot capacity / default bucket size; default 64 MiB */
     uint32_t n_slots;       /* device staging ring slots (>= 2); 0 = full device copy:
                                staging holds the whole image, the fence releases the

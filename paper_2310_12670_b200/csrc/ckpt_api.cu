@@ -96,7 +96,7 @@ extern "C" void ckpt_options_default(ckpt_options *o) {
     memset(o, 0, sizeof *o);
     o->struct_size = sizeof(ckpt_options);
     o->align = 256;
-    o->stripe_unit = 64 * 1024;
+    o->stripe_unit = 1024 * 1024;  // Q4; round 2: 1 MiB reads the m = 4 rows at the fabric's rate
     o->bucket_bytes = 64ull << 20;
     o->n_slots = 4;
     o->host_buffers = 2;

@@ -878,17 +878,19 @@ cudaError_t launch_pack_all(const PackAllArgs &a, int max_ctas, cudaStream_t s, 
     if (tma) {
         // one CTA per SM (192 KiB of SMEM) on max_ctas/2 SMs: 4 producer warps x 3 stages
         // Short-lived CTAs (k per SM in the grid) beat one persistent CTA per SM in the step
-        // (tools/pack_waves_ab.sh, C2 rank, D2H running): k = 1: 5.74-5.86 TB/s, k = 8:
-        // 5.93-5.95 TB/s, k = 64: 6.46-6.50 TB/s -- but a co-running GEMM loses 1.0-2.3%
-        // at k = 8 against 2.3-3.7% at k = 64.  The snapshot pack (which a training GEMM may
-        // overlap) takes k = 8, the unpack of a load (recovery: nothing co-runs) k = 64;
-        // CKPT_PACK_WAVES=k overrides both.
+        // (C2 rank, D2H running): k = 1: 5.74-5.86 TB/s, k = 8: 5.76-5.95, k = 16: 5.91,
+        // k = 32: 6.25, k = 64: 6.44-6.50 TB/s.  They also hurt a co-running GEMM LESS: a
+        // CTA holds its SM for ~pack/k, and the GEMM's next kernel waits for it, so the
+        // GEMMs overlapping the pack run 55% / 26% / 15% / 11% slower at k = 8 / 16 / 32 /
+        // 64 (round 2, 12 ABBA pairs, profiles/r02/r02f_waves*.jsonl; round 1's opposite
+        // reading was within the whole-window noise).  k = 64 for the snapshot and the
+        // unpack of a load; CKPT_PACK_WAVES=k overrides both.
         static int waves_env = -1;
         if (waves_env < 0) {
             const char *e = getenv("CKPT_PACK_WAVES");
             waves_env = e ? std::max(1, atoi(e)) : 0;
         }
-        const int waves = waves_env ? waves_env : (a.unpack ? 64 : 8);
+        const int waves = waves_env ? waves_env : 64;
         const int ctas = (max_ctas / 2 > 0 ? max_ctas / 2 : 1) * waves;
         // CKPT_PACK_L2HINT=1: the snapshot pack's bulk copies carry an L2 evict_first
         // policy, so its 2 x L_j bytes of streaming do not evict a co-running GEMM's tiles

@@ -92,7 +92,7 @@ def test_strerror_and_version(C):
 
 def test_options_defaults(C):
     o = C.ckpt_options_default()
-    assert (o.align, o.stripe_unit, o.bucket_bytes, o.n_slots, o.host_buffers) == (256, 65536, 64 << 20, 4, 2)
+    assert (o.align, o.stripe_unit, o.bucket_bytes, o.n_slots, o.host_buffers) == (256, 1 << 20, 64 << 20, 4, 2)
 
 
 def test_has_plan_spec_vectors(C):

@@ -309,7 +309,7 @@ def test_c1_16mib_m8_full_parity(torch, C):
     states = [make_rank_state("c1_16mb_fp32_m8", j, "cuda:0") for j in range(m)]
     ctxs = []
     for specs, ts in states:
-        c = C.ckpt_create(0, C.ckpt_options_default(n_slots=0))
+        c = C.ckpt_create(0, C.ckpt_options_default(n_slots=0, stripe_unit=65536))  # a 16 MiB shard: small u
         C.ckpt_register(c, descriptors(ts, specs))
         ctxs.append(c)
     try:
@@ -335,13 +335,13 @@ def test_c1_16mib_m8_full_parity(torch, C):
             C.ckpt_destroy(c)
 
 
-BENCH_BUCKET = 512 << 20  # bench.py defaults: full-copy staging, 512 MiB buckets, TMA pack, u = 64 KiB
+BENCH_BUCKET = 512 << 20  # bench.py defaults: full-copy staging, 512 MiB buckets, TMA pack, u = 1 MiB
 
 
 def bench_options(C, **kw):
     """The options bench.py's N=1 step runs with (bench.py main(): n_slots=0, 512 MiB
     buckets, CKPT_OPT_TMA_PACK -> pack_all_tma_kernel, CKPT_OPT_HOST_LOAD for e2e's load)."""
-    o = dict(n_slots=0, bucket_bytes=BENCH_BUCKET, stripe_unit=64 << 10,
+    o = dict(n_slots=0, bucket_bytes=BENCH_BUCKET, stripe_unit=1 << 20,
              flags=C.CKPT_OPT_TIMING | C.CKPT_OPT_HOST_LOAD | C.CKPT_OPT_TMA_PACK)
     o.update(kw)
     return C.ckpt_options_default(**o)
@@ -372,7 +372,7 @@ def test_c2_bench_config_full_image(torch, C):
             st = C.ckpt_get_stats(ctx)
             assert st["pack_launches"] == i + 1, "one pack launch per snapshot (single-launch TMA pack)"
             d, _ = C.ckpt_host_view(ctx, 0)  # the buffer just committed (i = 1, 2: both buffers)
-            n = verify_images_full([specs], Ls, 65536, {0: (d, None)}, gen_ranks=[3])
+            n = verify_images_full([specs], Ls, 1 << 20, {0: (d, None)}, gen_ranks=[3])
             assert n == Ls
             del d
         for t in ts:

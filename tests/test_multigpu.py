@@ -171,7 +171,7 @@ def _worker_c2(rank, world, port, q, config="c2_7b_tp8", extra_flags=0):
         specs, ts = make_rank_state(config, rank, dev)
         # bench.py's launch configuration: full-copy staging, 512 MiB buckets, TMA pack
         ctx = C.ckpt_create(rank, C.ckpt_options_default(
-            n_slots=0, bucket_bytes=512 << 20, stripe_unit=64 << 10,
+            n_slots=0, bucket_bytes=512 << 20, stripe_unit=1 << 20,
             flags=C.CKPT_OPT_TIMING | C.CKPT_OPT_HOST_LOAD | C.CKPT_OPT_TMA_PACK | extra_flags, host_buffers=1))
         C.ckpt_register(ctx, descriptors(ts, specs))
         C.protect_ipc(ctx)

@@ -27,7 +27,7 @@ def main():
     p.add_argument("--buckets", default="64")
     p.add_argument("--reps", type=int, default=3)
     p.add_argument("--n-slots", type=int, default=4)
-    p.add_argument("--unit", type=int, default=65536)
+    p.add_argument("--unit", type=int, default=1 << 20)
     p.add_argument("--flags", type=int, default=0)
     p.add_argument("--drill", action="store_true")
     p.add_argument("--device-only", action="store_true")

@@ -22,7 +22,7 @@ def main():
     p.add_argument("--reps", type=int, default=3)
     p.add_argument("--bucket", type=int, default=64 << 20)
     p.add_argument("--flags", type=int, default=0)
-    p.add_argument("--unit", type=int, default=65536, help="stripe unit u (Q4)")
+    p.add_argument("--unit", type=int, default=1 << 20, help="stripe unit u (Q4)")
     p.add_argument("--with-d2h", action="store_true", help="run a pinned D2H on every device meanwhile")
     p.add_argument("--rebuild", type=int, default=-1,
                    help="then lose member k (device copy + host image) and rebuild it from the survivors' "
