@@ -83,6 +83,21 @@ def _worker(rank, world, port, case, q):
         q.put((rank, None, traceback.format_exc()))
 
 
+def _retry_port_clash(fn):
+    """_free_port closes the socket before the workers' TCPStore binds it, so another
+    process can take the port in between (seen once in 25 cases: EADDRINUSE inside
+    init_process_group, before any work): run the case again on a fresh port."""
+    def wrapped(*a, **kw):
+        for attempt in range(3):
+            try:
+                return fn(*a, **kw)
+            except AssertionError as e:
+                if "EADDRINUSE" not in str(e) or attempt == 2:
+                    raise
+    return wrapped
+
+
+@_retry_port_clash
 def _run(world, case, timeout=300):
     import queue
     import time
@@ -547,6 +562,7 @@ def _aor_worker(rank, world, port, q):
         q.put((rank, None, traceback.format_exc()))
 
 
+@_retry_port_clash
 def _run_fn(fn, world, timeout=300):
     import queue
     import time
