@@ -55,6 +55,7 @@ def parse():
     p.add_argument("--scheme", default="aec", choices=["aec", "arc", "arc_aec"],
                    help="protection: AEC parity (default), ARC ring copies, or both (collaborative)")
     p.add_argument("--no-corun", action="store_true", help="skip the co-running GEMM measurement")
+    p.add_argument("--corun-pairs", type=int, default=12, help="A/B window pairs of the co-run measurement")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--cpu-seconds", type=float, default=12.0)
@@ -555,7 +556,7 @@ def main():
 
     corun = None
     if not a.no_corun:
-        corun = {"this_config": gemm_corun(torch, C, ctx, stream, a.bucket, barrier, allmax, dev)}
+        corun = {"this_config": gemm_corun(torch, C, ctx, stream, a.bucket, barrier, allmax, dev, a.corun_pairs)}
     C.ckpt_destroy(ctx)  # one context (and one pinned arena) alive at a time
     ctx = None
     if not a.no_corun and a.pack != "ce" and not a.device_only:
@@ -571,7 +572,7 @@ def main():
             C.protect_ipc(ctx2, group=sub)
         else:
             C.ckpt_protect(ctx2, 1, 0)
-        corun["ce_pack"] = gemm_corun(torch, C, ctx2, stream, a.bucket, barrier, allmax, dev)
+        corun["ce_pack"] = gemm_corun(torch, C, ctx2, stream, a.bucket, barrier, allmax, dev, a.corun_pairs)
         C.ckpt_destroy(ctx2)
     if corun:  # headline: the configuration whose throughput is the headline (both reported)
         corun["slowdown_pct"] = corun["this_config"]["slowdown_pct"]
