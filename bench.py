@@ -56,6 +56,8 @@ def parse():
                    help="protection: AEC parity (default), ARC ring copies, or both (collaborative)")
     p.add_argument("--no-corun", action="store_true", help="skip the co-running GEMM measurement")
     p.add_argument("--corun-pairs", type=int, default=12, help="A/B window pairs of the co-run measurement")
+    p.add_argument("--no-paper-shape", action="store_true",
+                   help="N=1: skip the extra short measurement of C4 (Llama-2-34B TP8, the paper's workload shape)")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--cpu-seconds", type=float, default=12.0)
@@ -578,6 +580,39 @@ def main():
         corun["slowdown_pct"] = corun["this_config"]["slowdown_pct"]
         corun["slowdown_pct_config"] = "this_config"
 
+    # N = 1: the paper's own workload shape (C4, Llama-2-34B TP8 stage-0 rank) in the same
+    # launch configuration, a few steps -- not the headline (BASELINE's metric is quoted on C2)
+    paper_shape = None
+    if world == 1 and not a.no_paper_shape and a.config != "c4_34b_tp8_stage0":
+        specs4, ts4 = make_rank_state("c4_34b_tp8_stage0", 0, dev)
+        S4 = sum(s.nbytes for s in specs4)
+        ctx4 = C.ckpt_create(local, C.ckpt_options_default(n_slots=a.n_slots, bucket_bytes=a.bucket, stripe_unit=a.unit,
+                                                           host_buffers=host_buffers, max_ctas=a.max_ctas, flags=flags))
+        C.ckpt_register(ctx4, descriptors(ts4, specs4))
+        C.ckpt_protect(ctx4, 1, 0)
+        for _ in range(2):
+            sid = C.ckpt_snapshot(ctx4, a.bucket, stream)
+            C.ckpt_wait(ctx4, sid)
+        C.ckpt_stats_reset(ctx4)
+        torch.cuda.synchronize()
+        f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        f0.record(stream)
+        for _ in range(3):
+            sid = C.ckpt_snapshot(ctx4, a.bucket, stream)
+            C.ckpt_wait(ctx4, sid)
+        f1.record(stream)
+        torch.cuda.synchronize()
+        t4 = f0.elapsed_time(f1) / 3
+        st4 = C.ckpt_get_stats(ctx4)
+        paper_shape = {"workload": "c4_34b_tp8_stage0", "state_bytes_per_gpu": S4, "tensors_per_gpu": len(specs4),
+                       "steps": 3, "ms_per_step": round(t4, 3), "value": round(S4 / t4 / 1e6, 3), "unit": "GB/s",
+                       "host_link_frac": round(st4["d2h_bytes"] / 3 / (t4 / 1e3) / 1e9 / d2h_peak, 4),
+                       "pack_gbs": round(st4["pack_bytes"] / st4["pack_ms"] / 1e6, 1) if st4["pack_ms"] else None,
+                       "pack_frac_of_hbm": round(st4["pack_bytes"] / st4["pack_ms"] / 1e6 / hbm_peak, 4)
+                       if st4["pack_ms"] else None}
+        C.ckpt_destroy(ctx4)
+        del ts4
+
     cpu = None
     if rank == 0 and world == 1 and not a.no_cpu_baseline:
         gbs, desc, _, _ = oracle_sample(a.config, 1, a.cpu_seconds, unit=a.unit)
@@ -617,7 +652,7 @@ def main():
             "roofline": roof, "other_kernels": others, "ce_mirror": ce_mirror,
             "gpu_launches": launches,
             "clocks": clocks,
-            "e2e": e2e, "cpu_baseline": cpu, "gemm_corun": corun,
+            "e2e": e2e, "cpu_baseline": cpu, "gemm_corun": corun, "paper_shape": paper_shape,
             "setup_s_rank0": round(t_setup, 2),
         }
         print(json.dumps(line), flush=True)
