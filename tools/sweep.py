@@ -35,6 +35,7 @@ def main():
     p.add_argument("--scheme", type=int, default=0, help="CKPT_SCHEME_*: 1 AEC, 2 ARC, 3 ARC+AEC")
     p.add_argument("--host-buffers", type=int, default=2)
     p.add_argument("--corun", action="store_true", help="bf16 GEMM co-run slowdown per bucket size (bench.py's)")
+    p.add_argument("--corun-pairs", type=int, default=12)
     p.add_argument("--max-ctas", default="0",
                    help="comma list of CTA budgets of the pack/XOR launches (0 = 2 x SMs); one record per budget")
     a = p.parse_args()
@@ -105,7 +106,7 @@ def main():
                "launches_per_snapshot": (st["pack_launches"] + st["xor_launches"]) // a.reps}
         if a.corun:
             import bench
-            co = bench.gemm_corun(torch, C, ctx, st0, bmib << 20, bar, amax, dev)
+            co = bench.gemm_corun(torch, C, ctx, st0, bmib << 20, bar, amax, dev, a.corun_pairs)
             rec["gemm_slowdown_pct"] = co["slowdown_pct"]
             rec["gemm_corun"] = {k: co[k] for k in ("whole_window", "in_window", "pack_window", "protect_window",
                                                     "snapshot_window", "clock_drop_pct", "sm_mhz", "power_w")}
