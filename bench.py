@@ -576,6 +576,25 @@ def main():
             C.ckpt_protect(ctx2, 1, 0)
         corun["ce_pack"] = gemm_corun(torch, C, ctx2, stream, a.bucket, barrier, allmax, dev, a.corun_pairs)
         C.ckpt_destroy(ctx2)
+        # the fine-grained configuration: a ring of 4 small slots (4 MiB buckets, or one
+        # stripe when that is larger) with the per-bucket TMA pack -- the C3 sweep at m = 4
+        # measured ~0% whole-window slowdown with 4 MiB buckets against 6.5-8% at 512 MiB
+        # (profiles/r02/r02l_c3_m4.jsonl); the tensors are released only after the last D2H
+        gm = G if world > 1 and G > 1 else 1
+        small = max(4 << 20, (gm - 1) * a.unit)
+        o3 = C.ckpt_options_default(n_slots=4, bucket_bytes=small, stripe_unit=a.unit, host_buffers=host_buffers,
+                                    flags=C.CKPT_OPT_TIMING | C.CKPT_OPT_HOST_LOAD | C.CKPT_OPT_TMA_PACK)
+        ctx3 = C.ckpt_create(local, o3)
+        C.ckpt_register(ctx3, descriptors(ts, specs))
+        if world > 1 and G > 1:
+            C.protect_ipc(ctx3, group=sub)
+        else:
+            C.ckpt_protect(ctx3, 1, 0)
+        corun["ring_small_buckets"] = gemm_corun(torch, C, ctx3, stream, small, barrier, allmax, dev, a.corun_pairs)
+        corun["ring_small_buckets"]["config"] = {"n_slots": 4, "bucket_bytes": small, "pack": "tma (per bucket)"}
+        corun["ring_small_buckets"]["state_gbs_per_gpu_alone"] = round(
+            S / (corun["ring_small_buckets"]["snapshot_ms_alone"] / 1e3) / 1e9, 3)
+        C.ckpt_destroy(ctx3)
     if corun:  # headline: the configuration whose throughput is the headline (both reported)
         corun["slowdown_pct"] = corun["this_config"]["slowdown_pct"]
         corun["slowdown_pct_config"] = "this_config"
