@@ -324,24 +324,6 @@ __device__ __forceinline__ void bulk_s2g(void *gmem, const void *smem, uint32_t 
     asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(gmem), "r"(smem_u32(smem)), "r"(bytes)
                  : "memory");
 }
-// Same, with an L2 cache policy (createpolicy): the streamed bytes are evicted first.
-__device__ __forceinline__ uint64_t l2_policy_evict_first() {
-    uint64_t p;
-    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
-    return p;
-}
-__device__ __forceinline__ void bulk_g2s_hint(void *smem, const void *gmem, uint32_t bytes, uint64_t *bar, uint64_t pol) {
-    asm volatile(
-        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
-            smem_u32(smem)),
-        "l"(gmem), "r"(bytes), "r"(smem_u32(bar)), "l"(pol)
-        : "memory");
-}
-__device__ __forceinline__ void bulk_s2g_hint(void *gmem, const void *smem, uint32_t bytes, uint64_t pol) {
-    asm volatile("cp.async.bulk.global.shared::cta.bulk_group.L2::cache_hint [%0], [%1], %2, %3;" ::"l"(gmem),
-                 "r"(smem_u32(smem)), "r"(bytes), "l"(pol)
-                 : "memory");
-}
 __device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
 template <int N>
 __device__ __forceinline__ void bulk_wait_read() {
@@ -456,14 +438,12 @@ struct BulkRing {
     uint8_t *smem;
     uint64_t *bars;
     uint32_t phase, issued, done;
-    uint64_t pol;  // 0: no cache hint; else an L2 policy for every bulk load and store
     Piece ring[NS];
     __device__ __forceinline__ void retire() {
         const uint32_t so = done % NS;
         mbar_wait(&bars[so], (phase >> so) & 1);
         phase ^= 1u << so;
-        if (pol) bulk_s2g_hint(ring[so].dst, smem + so * kTmaStage, ring[so].bytes, pol);
-        else bulk_s2g(ring[so].dst, smem + so * kTmaStage, ring[so].bytes);
+        bulk_s2g(ring[so].dst, smem + so * kTmaStage, ring[so].bytes);
         bulk_commit();
         ++done;
     }
@@ -473,8 +453,7 @@ struct BulkRing {
         if (issued >= NS) bulk_wait_read_n(done + NS - 1 - issued);
         ring[st] = Piece{s, d, bytes};
         mbar_expect_tx(&bars[st], bytes);
-        if (pol) bulk_g2s_hint(smem + st * kTmaStage, s, bytes, &bars[st], pol);
-        else bulk_g2s(smem + st * kTmaStage, s, bytes, &bars[st]);
+        bulk_g2s(smem + st * kTmaStage, s, bytes, &bars[st]);
         ++issued;
     }
     __device__ __forceinline__ void drain() {
@@ -495,7 +474,6 @@ __global__ void __launch_bounds__(32 * W) pack_all_tma_kernel(const __grid_const
     R.smem = smem + (size_t)w * NS * kTmaStage;
     R.bars = bars[w];
     R.phase = R.issued = R.done = 0;
-    R.pol = g.l2_evict_first ? l2_policy_evict_first() : 0;
     if (lane == 0) {
         for (int i = 0; i < NS; ++i) mbar_init(&bars[w][i], 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -892,16 +870,7 @@ cudaError_t launch_pack_all(const PackAllArgs &a, int max_ctas, cudaStream_t s, 
         }
         const int waves = waves_env ? waves_env : 64;
         const int ctas = (max_ctas / 2 > 0 ? max_ctas / 2 : 1) * waves;
-        // CKPT_PACK_L2HINT=1: the snapshot pack's bulk copies carry an L2 evict_first
-        // policy, so its 2 x L_j bytes of streaming do not evict a co-running GEMM's tiles
-        static int l2hint_env = -1;
-        if (l2hint_env < 0) {
-            const char *e = getenv("CKPT_PACK_L2HINT");
-            l2hint_env = e ? (atoi(e) != 0) : 0;
-        }
-        PackAllArgs b = a;
-        b.l2_evict_first = !a.unpack && l2hint_env;
-        return launch_pack_all_tma<3, 4>(b, ngroups, ctas, s);
+        return launch_pack_all_tma<3, 4>(a, ngroups, ctas, s);
     }
     const uint64_t g = ngroups < (uint64_t)max_ctas ? ngroups : (uint64_t)max_ctas;
     pack_all_kernel<<<(unsigned)g, kPackThreads, 0, s>>>(a);

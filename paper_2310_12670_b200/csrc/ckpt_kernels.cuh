@@ -82,8 +82,6 @@ struct PackAllArgs {
     uint32_t seq_base;
     uint32_t maxb;
     int unpack;            // 1: the load direction (image -> tensors), nothing is published
-    int l2_evict_first;    // bulk loads and stores carry an L2 evict_first policy (the
-                           // streamed bytes are not reused; a co-running GEMM's L2 tiles are)
 };
 
 

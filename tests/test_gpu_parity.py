@@ -876,8 +876,7 @@ def test_c_program_drill(torch, C, tmp_path, m, lost):
     assert r.stdout.strip() == f"ok m={m} lost={lost}"
 
 
-@pytest.mark.parametrize("knob", ["CKPT_XOR_IMPL=lsu", "CKPT_XOR_IMPL=tma", "CKPT_PACK_WAVES=1", "CKPT_PACK_WAVES=64", "CKPT_XOR_CTAS=296",
-                                  "CKPT_PACK_L2HINT=1"])
+@pytest.mark.parametrize("knob", ["CKPT_XOR_IMPL=lsu", "CKPT_XOR_IMPL=tma", "CKPT_PACK_WAVES=1", "CKPT_PACK_WAVES=64", "CKPT_XOR_CTAS=296"])
 def test_every_tuning_knob_stays_bit_exact(torch, C, knob):
     """Every environment tuning knob (read once per process, hence a subprocess) under the
     group encode and drill parity tests (every m, unit, staging mode and flag set, incl. the
