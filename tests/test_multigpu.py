@@ -51,7 +51,11 @@ def _worker(rank, world, port, case, q):
             off, _ = oracle.layout([s.nbytes for s in sp])
             imgs.append(oracle.pack(tb, off, g["L_star"]))
         P = oracle.encode(imgs, g["unit"], rank)
-        d, p = C.ckpt_host_view(ctx, 0, copy=True)
+        dev_only = bool(flags & C.CKPT_OPT_DEVICE_ONLY)  # no host image: the drill checks the tensors
+
+        def view():
+            return (imgs[rank], P) if dev_only else C.ckpt_host_view(ctx, 0, copy=True)
+        d, p = view()
         ok = [bool(np.array_equal(d, imgs[rank])), bool(np.array_equal(p, P))]
         # drill: every rank k in turn is lost (tensors + host image), rebuilt, reloaded
         for k in range(world):
@@ -64,7 +68,7 @@ def _worker(rank, world, port, case, q):
             C.ckpt_rebuild(ctx, k)
             C.ckpt_load(ctx)
             torch.cuda.synchronize()
-            d, p = C.ckpt_host_view(ctx, 0, copy=True)
+            d, p = view()
             good = np.array_equal(d, imgs[rank]) and np.array_equal(p, P)
             for t, x in enumerate(ts):
                 got = x.contiguous().view(torch.uint8).cpu().numpy()
@@ -73,7 +77,7 @@ def _worker(rank, world, port, case, q):
         # a second snapshot after the drill still commits and matches
         sid = C.ckpt_snapshot(ctx)
         C.ckpt_wait(ctx, sid)
-        d, p = C.ckpt_host_view(ctx, 0, copy=True)
+        d, p = view()
         ok.append(bool(np.array_equal(d, imgs[rank]) and np.array_equal(p, P)))
         C.ckpt_destroy(ctx)
         dist.barrier()
@@ -155,6 +159,7 @@ def _world():
     ("tiny_5", 4096, 0, 1 << 16, 0x800, 1),  # CKPT_OPT_REBUILD_SELF (the default at m >= 3 is shares)
     ("tiny_7", 4096, 0, 1 << 20, 0x400, 1),  # CKPT_OPT_XOR_PUSH: bulk XOR reductions over NVLink
     ("tiny_6", 16, 0, 1 << 16, 0x600, 0),
+    ("tiny_9", 4096, 0, 1 << 16, 0x20, 1),   # DEVICE_ONLY: the encode of bucket k overlaps the packs
 ])
 def test_ipc_group_all_gpus(case):
     _run(min(_world(), 8), case)
