@@ -511,15 +511,14 @@ int stage_xor_all(ckpt_ctx *c) {
     return sig_signal(c, c->sX, kRel, bucket_seq(c, c->op_NB - 1), slot_of(c, c->op_NB - 1));
 }
 
-// DEVICE_ONLY (protection in HBM): the parity IS the critical path, so the encode of
-// bucket k starts as soon as every member published bucket k, overlapping the packs
-// (per-bucket launches) instead of one launch after the whole pack.  With the D2H the
-// parity is off the critical path and one launch after this member's pack avoids
-// splitting HBM between the two.
-bool xor_overlaps_pack(const ckpt_ctx *c) { return device_only(c) && !(c->opt.flags & CKPT_OPT_XOR_PUSH); }
-
+// One encode launch over the whole image after this member's pack, also in DEVICE_ONLY
+// mode where the parity is the critical path: round 2 tried per-bucket launches that start
+// as soon as every member published bucket k (overlapping the packs), and the N=2
+// device-only step got SLOWER (21.86 vs 21.30 ms): each 512 MiB launch ran at 575 GB/s
+// against 675 for the single launch (pipeline fill and drain per launch, gaps at the
+// READY waits), which ate the 3.5 ms of overlap (profiles/r02/r02p_n2_dev.jsonl).
 bool xor_in_one_launch(const ckpt_ctx *c) {
-    return c->m >= 2 && c->aec && single_launch(c) && !(c->opt.flags & CKPT_OPT_CE_GATHER) && !xor_overlaps_pack(c);
+    return c->m >= 2 && c->aec && single_launch(c) && !(c->opt.flags & CKPT_OPT_CE_GATHER);
 }
 
 bool xor_push(const ckpt_ctx *c) { return (c->opt.flags & CKPT_OPT_XOR_PUSH) && xor_in_one_launch(c); }
@@ -596,7 +595,7 @@ int stage_xor(ckpt_ctx *c, uint64_t k) {
     // Row me reads only the peers' units.  After a single-launch pack the XOR also waits
     // for this rank's own pack: the two would otherwise split HBM/NVLink bandwidth while
     // the parity is not on the critical path (its D2H is queued after all the data).
-    if (single_launch(c) && k == 0 && !xor_overlaps_pack(c)) CUDA_TRY(cudaStreamWaitEvent(c->sX, c->ev_pack_all, 0));
+    if (single_launch(c) && k == 0) CUDA_TRY(cudaStreamWaitEvent(c->sX, c->ev_pack_all, 0));
     if ((rc = wait_all(c, c->sX, kReady, bucket_seq(c, k), s))) return rc;
     if (ring_reuse(c, k)) CUDA_TRY(cudaStreamWaitEvent(c->sX, c->ev_d2h_par[s], 0));
     if ((rc = do_encode(c, k, c->sX))) return rc;

@@ -159,7 +159,7 @@ def _world():
     ("tiny_5", 4096, 0, 1 << 16, 0x800, 1),  # CKPT_OPT_REBUILD_SELF (the default at m >= 3 is shares)
     ("tiny_7", 4096, 0, 1 << 20, 0x400, 1),  # CKPT_OPT_XOR_PUSH: bulk XOR reductions over NVLink
     ("tiny_6", 16, 0, 1 << 16, 0x600, 0),
-    ("tiny_9", 4096, 0, 1 << 16, 0x20, 1),   # DEVICE_ONLY: the encode of bucket k overlaps the packs
+    ("tiny_9", 4096, 0, 1 << 16, 0x20, 1),   # DEVICE_ONLY over IPC (protection in HBM, drill checks tensors)
 ])
 def test_ipc_group_all_gpus(case):
     _run(min(_world(), 8), case)
