@@ -287,7 +287,8 @@ int ckpt_fence(ckpt_ctx *ctx, uint64_t id, void *stream);
 int ckpt_wait(ckpt_ctx *ctx, uint64_t id);
 
 /* Non-blocking: *done = 1 when snapshot `id` has landed everywhere ckpt_wait waits for
- * (ckpt_wait then returns at once and commits), else 0.  Never commits by itself.
+ * (ckpt_wait then returns at once and commits), else 0.  Never commits by itself.  With
+ * CKPT_OPT_WINDOWED it also enqueues the next window-gated copies (see ckpt_window).
  * Errors: EINVAL, ESTATE (unknown id), ECUDA. */
 int ckpt_test(ckpt_ctx *ctx, uint64_t id, int *done);
 
@@ -384,7 +385,12 @@ int ckpt_arena_unlink(uint64_t key, uint32_t m, uint32_t nbuf);
  * the first bubble_bytes of the image (whole buckets) go out only in bubbles, the rest
  * alongside computation or in a bubble (reading Q26); by default every bucket is a bubble
  * bucket.  Buckets leave in image order.  A snapshot whose windows are
- * never reopened does not complete (ckpt_wait times out). */
+ * never reopened does not complete (ckpt_wait times out; ckpt_destroy opens every window
+ * before it drains).  With one process per member (IPC groups, or no group) the gated
+ * copies are enqueued progressively -- at most 32 beyond the last one that completed --
+ * so ckpt_snapshot never blocks the training thread on a full stream queue; ckpt_window,
+ * ckpt_test and ckpt_wait enqueue the next ones, so call them while the snapshot is in
+ * flight (a training loop that opens windows does). */
 #define CKPT_WINDOW_BUBBLE  0x1u
 #define CKPT_WINDOW_COMPUTE 0x2u
 #define CKPT_WINDOW_COMM    0x4u  /* Layer 3 (P.425): a communication phase of training on
