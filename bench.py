@@ -206,15 +206,21 @@ class OracleGroup:
                      f"{threads} windows x {self.W / 2**20:.0f} MiB of each of {m} member(s) of {config}, one "
                      f"window per host thread ({threads} threads, each the unchanged 1-thread oracle)")
 
-    def run(self) -> float:
+    def run(self, keep: bool = False) -> float:
+        """One timed pass; with keep, self.out[i] = (images, parity rows, rebuilt member 0)
+        of window i (the CPU test checks them against the oracle on whole images)."""
         import threading
         o, m, u = self.oracle, self.m, self.u
+        self.out = [None] * self.threads
 
         def one(i):
             Ds = [o.pack(ps, wh, self.W) for ps, wh in self.work[i]]
+            Ps = R = None
             if m > 1:
                 Ps = [o.encode(Ds, u, r) for r in range(m)]
-                o.rebuild([None] + Ds[1:], [None] + Ps[1:], u, 0, [True] + [False] * (m - 1))
+                R = o.rebuild([None] + Ds[1:], [None] + Ps[1:], u, 0, [True] + [False] * (m - 1))
+            if keep:
+                self.out[i] = (Ds, Ps, R)
 
         th = [threading.Thread(target=one, args=(i,)) for i in range(self.threads)]
         t0 = time.perf_counter()
