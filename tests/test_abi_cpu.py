@@ -70,7 +70,7 @@ def test_plan_random_vs_oracle(C):
         assert C.ckpt_plan_layout(sizes, align) == oracle.layout(sizes, align)
         m = int(rng.integers(1, 9))
         Ls = rng.integers(1, 1 << 24, size=m).tolist()
-        u = int(rng.choice([0, 16, 4096, 65536]))
+        u = int(rng.choice([0, 16, 4096, 65536, 1 << 20]))  # 1 MiB: the default since round 2
         assert C.ckpt_plan_common(Ls, u) == oracle.common_length(Ls, u)
 
 
