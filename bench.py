@@ -87,7 +87,7 @@ class Clocks:
          "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
          "clocks_event_reasons.sw_power_cap")
 
-    def __init__(self, gpu: int):
+    def __init__(self, gpu):
         self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
         try:
             self.p = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
@@ -449,7 +449,8 @@ def main():
     C.ckpt_stats_reset(ctx)
     barrier()
     torch.cuda.synchronize()
-    clk = Clocks(local)
+    p_ = torch.cuda.get_device_properties(dev)  # nvidia-smi -i by PCI bus id: immune to CUDA_VISIBLE_DEVICES
+    clk = Clocks(f"{p_.pci_domain_id:08X}:{p_.pci_bus_id:02X}:{p_.pci_device_id:02X}.0")
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(stream)
     for _ in range(a.steps):
