@@ -44,3 +44,24 @@ def test_oracle_group_windows_are_slices_of_the_whole_image(m, unit, threads):
             for r in range(m):
                 assert np.array_equal(Pw[r], Ps[r][a // (m - 1):b // (m - 1)]), f"window {i} parity row {r}"
             assert np.array_equal(R, imgs[0][a:b]), f"window {i} rebuild of member 0"
+
+
+def test_reference_arm_prints_the_contract_line():
+    """`bench.py --impl reference` (the oracle as the reference arm, no GPU needed): one JSON
+    line with the base contract's keys, impl=reference, a cpu_baseline describing the run
+    and a zero-copy e2e; under torchrun only rank 0 prints (here: one process)."""
+    import json
+    import subprocess
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference", "--steps", "1",
+                        "--warmup", "0", "--cpu-seconds", "0.5", "--config", "c1_16mb_fp32_m8"],
+                       cwd=ROOT, capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = [x for x in r.stdout.splitlines() if x.startswith("{")]
+    assert len(lines) == 1
+    d = json.loads(lines[0])
+    for k in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better", "scaling",
+              "vs_baseline", "dtype", "data", "config", "impl", "cpu_baseline", "e2e"):
+        assert k in d, k
+    assert d["impl"] == "reference" and d["value"] > 0 and d["unit"] == "GB/s"
+    assert d["cpu_baseline"]["kind"] == "oracle" and d["cpu_baseline"]["value"] == d["value"]
+    assert d["e2e"] == {"value": d["value"], "unit": d["unit"], "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}
